@@ -1,0 +1,207 @@
+/*
+ * vpetabc.h -- C ABI of libvpetabc.so, the B200 (sm_100a) implementation of the
+ * data-parallel hot path of vPET-ABC (arxiv 2603.14859): voxelwise rejection ABC.
+ *
+ * Citation key: P:n = line n of the paper's LaTeX source, with the
+ * equation / algorithm label; S:n = SPEC.md line n; DESIGN.md Rk = reading k.
+ *
+ * What one call of abc_run_voxels computes (Alg. 1 "Vectorized Voxelwise Rejection
+ * ABC"):
+ *   line 1-2  draws i = 0..N-1 of (model m_i, theta_i) from the priors
+ *   line 3    model curves s_i = frame averages of the model TAC
+ *   line 4    D_ji = rho(y_j, s_i) for every voxel j
+ *   line 5    per voxel the n smallest D_ji (top-n) or
+ *             every draw with D_ji <= eps
+ *   then      posterior summaries: model probabilities, the
+ *             preferred model (>50 %), conditional mean / SD / quantiles
+ *              and K_i = K1 k3/(k2+k3).
+ * Results equal those of the FP64 CPU oracle (oracle/) on the same inputs: the
+ * GPU ranks draws with an FP32 pass whose error is bounded, then re-scores every
+ * candidate near the acceptance boundary in FP64 exactly as the oracle does
+ * (DESIGN.md "Exactness").
+ *
+ * Conventions
+ *   Ownership:  every input is caller-owned and copied (or only read) during the
+ *               call; outputs are caller-allocated; the context is library-owned
+ *               and released by abc_destroy.
+ *   Errors:     status codes only; nothing is thrown and nothing exits across the
+ *               ABI.  abc_last_error(ctx) describes the last failure on ctx and is
+ *               valid until the next call on ctx.
+ *   Threading:  a context is bound to one device and is not re-entrant; use one
+ *               context per device / host thread.
+ *   State:      abc_init -> {abc_set_input_function, abc_set_frames} (any order,
+ *               repeatable) -> abc_run_voxels* ; running before both are set gives
+ *               ABC_E_STATE.
+ *   Units:      time in minutes, rates in 1/min, activity in any consistent unit.
+ *   Multi-GPU:  the ABI is per device; voxel sharding and NCCL live above it
+ *               (paper_2603_14859_b200/distributed.py).
+ */
+#ifndef VPETABC_H
+#define VPETABC_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VPETABC_ABI_VERSION 1
+#define ABC_MAX_P 8       /* parameter columns per draw (2TCM family uses 5, RT family 7) */
+#define ABC_MAX_MODELS 4  /* M */
+#define ABC_MAX_L 128     /* frames per TAC */
+
+typedef enum {
+  ABC_OK = 0,
+  ABC_E_ARG = 1,          /* invalid argument (see each function) */
+  ABC_E_STATE = 2,        /* input function or frames not set */
+  ABC_E_NOMEM = 3,        /* device memory for this call exceeds what is free; nothing allocated */
+  ABC_E_CUDA = 4,         /* a CUDA runtime error; abc_last_error has the CUDA message */
+  ABC_E_UNSUPPORTED = 5   /* valid request outside what this build supports */
+} abc_status;
+
+/* Forward models.  Parameter columns:
+ *   2TCM family:  [K1, k2, k3, k4, Vb]            -- IRR forces k4 = 0
+ *   RT family:  [R1, k2, k2a, gamma, tD, tP, alpha]
+ *                            -- MRTM forces gamma = 0; tD, tP, alpha do not exist
+ *                               for MRTM (their summaries are NaN).  Column 5 is drawn as
+ *                               the offset tP - tD ~ U(lo[5], hi[5]) and reported as
+ *                               tP = tD + offset (R8).
+ * All models of one context must be of the same family. */
+typedef enum { ABC_2TCM_IRR = 0, ABC_2TCM_REV = 1, ABC_MRTM = 2, ABC_LPNTPET = 3 } abc_model_kind;
+
+/* Discrepancy (Alg.1 l.4): WL2: D = sum_f w_f (y_f - s_f)^2 (north star);
+ * L1: D = sum_f w_f |y_f - s_f|.  Exactly the oracle's FP64 value. */
+typedef enum { ABC_DIST_L1 = 1, ABC_DIST_WL2 = 2 } abc_distance;
+
+/* Acceptance: TOPN keeps the n smallest by (D, draw index) (ties -> lower
+ * index); EPS keeps every draw with D <= epsilon. */
+typedef enum { ABC_ACCEPT_TOPN = 0, ABC_ACCEPT_EPS = 1 } abc_accept;
+
+/* Input function.  PWL: knots (t_k, c_k), t_0 = 0, t strictly increasing, linear in
+ * between, held at c_last after the last knot (IDIF "frame-wise mean"; R1).
+ * FENG: value[6] = (beta1, beta2, beta3, kappa1, kappa2, kappa3) of P:204-207, kappas > 0.
+ * 2TCM: the input is the plasma curve C_p (= C_wb).  RT models: the input is the
+ * reference-region TAC C_r and must be PWL. */
+typedef enum { ABC_INPUT_PWL = 0, ABC_INPUT_FENG = 1 } abc_input_kind;
+
+/* abc_config.flags */
+#define ABC_FLAG_TIMING 0x1u     /* record per-stage CUDA-event times (abc_get_stats) */
+#define ABC_FLAG_EXACT 0x2u      /* skip the FP32 pass: exact FP64 scan for every voxel (slow) */
+#define ABC_FLAG_COUNT_WORK 0x4u /* count executed frame updates of the FP32 pass */
+#define ABC_FLAG_NO_PRUNE 0x8u   /* FP32 pass evaluates all frames of every pair (A/B only) */
+#define ABC_FLAG_NO_REORDER 0x10u/* FP32 pass keeps the acquisition frame order (A/B only) */
+
+/* abc_run_voxels ptr_flags */
+#define ABC_PTR_TACS_DEVICE 0x1u /* tacs is a device pointer on ctx's device */
+#define ABC_PTR_OUT_DEVICE 0x2u  /* every abc_result array is a device pointer */
+
+typedef struct abc_model_spec {
+  int32_t kind;           /* abc_model_kind */
+  uint32_t reserved0;     /* must be 0 */
+  uint64_t n_draws;       /* N_m >= 1: this model owns the contiguous draw-index block
+                             [sum_{k<m} N_k, sum_{k<=m} N_k)  (Alg.1 l.1; R7) */
+  float lo[ABC_MAX_P];    /* uniform prior U(lo, hi) per column; lo == hi fixes the column */
+  float hi[ABC_MAX_P];
+} abc_model_spec;
+
+typedef struct abc_config {
+  uint32_t struct_size;   /* = sizeof(abc_config) (376) */
+  uint32_t n_models;      /* M, 1..ABC_MAX_MODELS */
+  uint64_t seed;          /* Philox4x32-10 key (R7) */
+  int32_t device;         /* CUDA device ordinal */
+  int32_t distance;       /* abc_distance */
+  int32_t accept;         /* abc_accept */
+  uint32_t n_accept;      /* n for TOPN: 1 <= n <= N, n <= 4096 (n = floor(N p)) */
+  double epsilon;         /* tolerance h for EPS, >= 0 */
+  double lpnt_step_min;   /* lp-ntPET integrator step delta (min); <= 0 selects 0.05 */
+  uint32_t flags;         /* ABC_FLAG_* */
+  uint32_t reserved1;     /* must be 0 */
+  abc_model_spec model[ABC_MAX_MODELS];
+} abc_config;
+
+/* Caller-allocated outputs (row-major).  A NULL pointer means "not produced".
+ * P = 5 for the 2TCM family, 7 for the RT family; M = n_models. */
+typedef struct abc_result {
+  float* prob;          /* J x M   count_m / n_acc (NaN if nothing accepted)             */
+  int32_t* preferred;   /* J       argmax_m count_m, ties -> lowest m (= the >50 % rule of
+                                   P:282 for M = 2 with model 0 the simpler model); -1 if none */
+  uint32_t* count;      /* J x M   accepted draws per model                                */
+  float* mean;          /* J x P   mean of each column over the accepted draws of the
+                                   preferred model; NaN if the column does not exist */
+  float* sd;            /* J x P   SD, ddof = 1 (NaN if < 2 draws)                          */
+  float* q;             /* J x P x 3  type-7 quantiles at 2.5/50/97.5 % (TOPN only, else NaN) */
+  float* ki_mean;       /* J       K_i = K1 k3/(k2+k3) per accepted draw (2TCM only)  */
+  float* ki_sd;         /* J                                                                 */
+  float* ki_q;          /* J x 3   (TOPN only)                                               */
+  uint64_t* acc_idx;    /* J x n   accepted draw indices sorted by (D, index) (TOPN only)    */
+  double* acc_dist;     /* J x n   their FP64 discrepancies (TOPN only)                      */
+} abc_result;
+
+/* Per-call statistics of the last abc_run_voxels on ctx (times need ABC_FLAG_TIMING). */
+typedef struct abc_stats {
+  uint32_t struct_size;       /* = sizeof(abc_stats) */
+  uint32_t gpu_launches;      /* kernels launched by the last run */
+  uint64_t n_voxels;
+  uint64_t n_draws;
+  uint64_t n_fallback;        /* voxels whose FP32 pass could not be certified (re-run exactly) */
+  uint64_t frame_updates;     /* executed FP32 frame updates (ABC_FLAG_COUNT_WORK) */
+  uint32_t lp;                /* padded frame count of the FP32 pass */
+  uint32_t heap_k;            /* candidates kept per voxel by the FP32 pass */
+  double ms_h2d, ms_bank, ms_order, ms_scan, ms_certify, ms_fallback, ms_d2h, ms_total;
+} abc_stats;
+
+typedef struct abc_ctx abc_ctx; /* opaque, library-owned */
+
+/* Create a context on cfg->device.  ABC_E_ARG: struct_size mismatch, M out of range,
+ * mixed model families, N_m = 0, N = sum N_m >= 2^32, lo > hi or non-finite bounds,
+ * 2TCM with lo[k3] <= 0 (R3), unknown distance/accept, TOPN with n = 0,
+ * n > N or n > 4096, EPS with epsilon < 0 or NaN, reserved fields != 0.
+ * ABC_E_CUDA: the device cannot be selected.  *out is NULL on failure. */
+abc_status abc_init(const abc_config* cfg, abc_ctx** out);
+
+/* Set the input function (host arrays, copied).  kind = ABC_INPUT_PWL: t_min[n], value[n],
+ * n >= 1, t_min[0] == 0, strictly increasing, finite.  kind = ABC_INPUT_FENG: value[6]
+ * (t_min ignored, n == 6), finite, kappas > 0; ABC_E_UNSUPPORTED for RT models. */
+abc_status abc_set_input_function(abc_ctx* ctx, int32_t kind, const double* t_min,
+                                  const double* value, uint32_t n);
+
+/* Set the frame schedule (host arrays, copied): L frames [start, start + dur), start >= 0,
+ * dur > 0, non-overlapping and increasing (start[f+1] >= start[f] + dur[f]), 1 <= L <= 128.
+ * weight (FP32, > 0, finite) may be NULL for w = 1 (R6). */
+abc_status abc_set_frames(abc_ctx* ctx, const double* start_min, const double* dur_min,
+                          const float* weight, uint32_t L);
+
+/* Run Alg. 1 for J voxels.  tacs: J x L FP32 row-major (frame-contiguous per voxel), host
+ * or device per ptr_flags; negative values allowed, non-finite values -> ABC_E_ARG.
+ * J = 0 is a no-op.  The work is ordered on the context's stream; the call returns after
+ * the results are complete (host outputs) or enqueued (device outputs, see abc_sync).
+ * ABC_E_NOMEM if the bank (2 x N x L FP32), the per-voxel state and the staging buffers
+ * do not fit in free device memory (checked before allocating). */
+abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t ptr_flags,
+                          abc_result* out);
+
+/* Model selection only: prob (J x M) and preferred (J). */
+abc_status abc_model_select(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t ptr_flags,
+                            float* prob, int32_t* preferred);
+
+/* Order the context's work on a caller stream (a cudaStream_t; NULL = the library's own
+ * stream).  The stream must belong to ctx's device and outlive its use. */
+abc_status abc_set_stream(abc_ctx* ctx, void* cuda_stream);
+
+/* Block until the context's stream is idle. */
+abc_status abc_sync(abc_ctx* ctx);
+
+/* Copy the statistics of the last run (stats->struct_size must be set). */
+abc_status abc_get_stats(const abc_ctx* ctx, abc_stats* stats);
+
+/* Copy rows [first, first + count) of the simulation bank of the last run (Alg.1 l.3, the
+ * N x L matrix X of P:150, FP32, acquisition frame order) to host memory out[count * L].
+ * ABC_E_STATE before the first run; ABC_E_ARG if the rows are out of range. */
+abc_status abc_get_bank(const abc_ctx* ctx, float* out, uint64_t first, uint64_t count);
+
+const char* abc_last_error(const abc_ctx* ctx);
+void abc_destroy(abc_ctx* ctx);
+uint32_t abc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VPETABC_H */

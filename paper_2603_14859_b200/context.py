@@ -1,0 +1,156 @@
+"""AbcContext: thin Python wrapper over one abc_ctx (one device)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi as A
+
+
+def family_width(kind: str) -> int:
+    """Parameter columns of a model family: 5 (2TCM: K1,k2,k3,k4,Vb), 7 (RT: R1,k2,k2a,gamma,tD,tP,alpha)."""
+    return 7 if kind in ("MRTM", "LPNTPET") else 5
+
+
+_DTYPES = {"prob": np.float32, "preferred": np.int32, "count": np.uint32, "mean": np.float32, "sd": np.float32,
+           "q": np.float32, "ki_mean": np.float32, "ki_sd": np.float32, "ki_q": np.float32, "acc_idx": np.uint64,
+           "acc_dist": np.float64}
+ALL_OUTPUTS = tuple(_DTYPES)
+
+
+class AbcContext:
+    def __init__(self, models, seed=2026, distance="WL2", accept="TOPN", n_accept=1, epsilon=0.0,
+                 lpnt_step_min=0.05, flags=0, device=0):
+        self._lib = A.load_library()
+        self.models = [dict(m) for m in models]
+        self.accept = accept
+        self.n_accept = int(n_accept)
+        self.device = int(device)
+        self.cfg = A.make_config(self.models, seed=seed, distance=distance, accept=accept, n_accept=n_accept,
+                                 epsilon=epsilon, lpnt_step_min=lpnt_step_min, flags=flags, device=device)
+        h = C.c_void_p()
+        st = self._lib.abc_init(C.byref(self.cfg), C.byref(h))
+        if st != 0:
+            raise A.AbcError(st, "abc_init rejected the configuration")
+        self._h = h
+        self.M = len(self.models)
+        self.P = family_width(self.models[0]["kind"])
+        self.N = sum(int(m["n_draws"]) for m in self.models)
+        self.L = None
+
+    # -- lifecycle --
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.abc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != 0:
+            raise A.AbcError(st, self._lib.abc_last_error(self._h).decode())
+
+    # -- configuration --
+    def set_input_function(self, kind, value, t=None):
+        v = np.ascontiguousarray(value, dtype=np.float64)
+        tt = None if t is None else np.ascontiguousarray(t, dtype=np.float64)
+        self._check(self._lib.abc_set_input_function(self._h, A.INPUTS[kind], None if tt is None else A.host_ptr(tt),
+                                                     A.host_ptr(v), len(v)))
+
+    def set_frames(self, start, dur, weight=None):
+        s = np.ascontiguousarray(start, dtype=np.float64)
+        d = np.ascontiguousarray(dur, dtype=np.float64)
+        w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float32)
+        self._check(self._lib.abc_set_frames(self._h, A.host_ptr(s), A.host_ptr(d),
+                                             None if w is None else A.host_ptr(w), len(s)))
+        self.L = len(s)
+
+    def set_stream(self, stream_handle):
+        """Order the context's work on a CUDA stream handle (e.g. torch.cuda.current_stream().cuda_stream)."""
+        self._check(self._lib.abc_set_stream(self._h, C.c_void_p(stream_handle) if stream_handle else None))
+
+    def sync(self):
+        self._check(self._lib.abc_sync(self._h))
+
+    def stats(self) -> dict:
+        s = A.Stats()
+        s.struct_size = C.sizeof(A.Stats)
+        self._check(self._lib.abc_get_stats(self._h, C.byref(s)))
+        return s.as_dict()
+
+    def bank(self, first=0, count=None):
+        """Rows of the last run's simulation bank (N x L, FP32) -- diagnostic copy to host."""
+        count = self.N - first if count is None else count
+        out = np.empty((count, self.L), dtype=np.float32)
+        self._check(self._lib.abc_get_bank(self._h, A.host_ptr(out), int(first), int(count)))
+        return out
+
+    # -- run --
+    def shapes(self, J):
+        M, P, n = self.M, self.P, self.n_accept
+        return {"prob": (J, M), "preferred": (J,), "count": (J, M), "mean": (J, P), "sd": (J, P), "q": (J, P, 3),
+                "ki_mean": (J,), "ki_sd": (J,), "ki_q": (J, 3), "acc_idx": (J, n), "acc_dist": (J, n)}
+
+    def run_voxels(self, tacs, want=ALL_OUTPUTS, out=None):
+        """Run Alg. 1 on a J x L float32 array.
+
+        tacs: numpy array (host) or torch CUDA tensor (device).  Outputs are numpy arrays for host
+        input and torch CUDA tensors for device input, unless `out` (dict of preallocated arrays /
+        tensors, all host or all device) is given.
+        """
+        is_torch = type(tacs).__module__.startswith("torch")
+        flags = 0
+        if is_torch:
+            import torch
+            if tacs.dtype != torch.float32 or not tacs.is_contiguous() or tacs.dim() != 2:
+                raise ValueError("tacs must be a contiguous 2-D float32 tensor")
+            J = int(tacs.shape[0])
+            tptr = C.c_void_p(tacs.data_ptr()) if J else None
+            if tacs.is_cuda:
+                flags |= A.PTR_TACS_DEVICE
+        else:
+            y = np.ascontiguousarray(tacs, dtype=np.float32)
+            if y.ndim != 2:
+                raise ValueError("tacs must be J x L")
+            J = y.shape[0]
+            tptr = A.host_ptr(y) if J else None
+        shapes = self.shapes(J)
+        want = [w for w in want if not (self.accept == "EPS" and w in ("acc_idx", "acc_dist"))]
+        res = {}
+        if out is not None:
+            res = dict(out)
+        elif is_torch and tacs.is_cuda:
+            import torch
+            tdt = {np.float32: torch.float32, np.int32: torch.int32, np.uint32: torch.int32,
+                   np.uint64: torch.int64, np.float64: torch.float64}
+            for name in want:
+                res[name] = torch.empty(shapes[name], dtype=tdt[_DTYPES[name]], device=tacs.device)
+        else:
+            for name in want:
+                res[name] = np.empty(shapes[name], dtype=_DTYPES[name])
+        r = A.Result()
+        dev_out = None
+        for name, arr in res.items():
+            if type(arr).__module__.startswith("torch"):
+                ptr = arr.data_ptr()
+                d = bool(arr.is_cuda)
+            else:
+                ptr = arr.ctypes.data
+                d = False
+            if dev_out is None:
+                dev_out = d
+            elif dev_out != d:
+                raise ValueError("outputs must be all host or all device")
+            setattr(r, name, ptr)
+        if dev_out:
+            flags |= A.PTR_OUT_DEVICE
+        self._check(self._lib.abc_run_voxels(self._h, tptr, J, flags, C.byref(r)))
+        return res
+
+    def model_select(self, tacs):
+        return self.run_voxels(tacs, want=("prob", "preferred"))

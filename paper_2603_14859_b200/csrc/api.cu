@@ -1,0 +1,746 @@
+// api.cu -- host runtime and C ABI of libvpetabc.so (see include/vpetabc.h).
+//
+// Owns the per-device context: validated configuration, draw-independent time grids and
+// frame tables (built here in FP64), device buffers (reused across calls), the stream, and
+// the launch sequence of one abc_run_voxels call:
+//   K0  finite check of the TACs
+//   K1  bank: N draws simulated in FP64, stored RN32            (Alg.1 l.1-3)
+//   K1b frame spread + scan order; K1c negated prescaled copy
+//   K2  FP32 pass: fused distance + per-voxel selection        (Alg.1 l.4-5)
+//   K3  FP64 certification, K4 posterior reduction
+//   K5  exact FP64 scan of uncertified voxels, then K3/K4 on them
+// Nothing runs on the CPU except validation and table construction.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace vpet;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+uint32_t family_width(int kind) { return kind >= ABC_MRTM ? 7u : 5u; }
+
+enum Stage { EV_START, EV_H2D, EV_BANK, EV_ORDER, EV_SCAN, EV_CERT, EV_FB, EV_D2H, EV_N };
+
+}  // namespace
+
+struct abc_ctx {
+  abc_config cfg{};
+  int dev = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t N = 0;
+  uint32_t P = 5, M = 1;
+  PriorDev prior{};
+  // input
+  bool have_input = false, have_frames = false;
+  int input_kind = ABC_INPUT_PWL;
+  double feng[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<double> kt, kc;
+  // frames
+  uint32_t L = 0;
+  std::vector<double> fs, fd;
+  std::vector<float> w;
+  bool unit_w = true;
+  // device tables
+  bool dirty = true;
+  uint32_t G = 0, GF = 0;
+  DevBuf d_fdur, d_fs, d_fe, d_favg, d_w, d_wsc, d_gt, d_gc, d_gframe, d_ft, d_fc, d_fframe;
+  // work buffers
+  DevBuf d_prior, bank, bankp, var, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
+  abc_stats stats{};
+  bool bank_valid = false;
+  uint32_t bank_L = 0;
+  cudaEvent_t ev[EV_N] = {};
+  bool ev_ok = false;
+};
+
+namespace {
+
+abc_status fail(abc_ctx* c, abc_status s, const std::string& m) {
+  if (c) c->err = m;
+  return s;
+}
+
+abc_status cuda_fail(abc_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, ABC_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                                 \
+  do {                                                           \
+    cudaError_t e_ = (call);                                     \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);     \
+  } while (0)
+
+template <class T>
+cudaError_t upload(DevBuf& b, const std::vector<T>& v) {
+  cudaError_t e = b.ensure(sizeof(T) * (v.empty() ? 1 : v.size()));
+  if (e != cudaSuccess) return e;
+  if (v.empty()) return cudaSuccess;
+  return cudaMemcpy(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
+}
+
+// PWL interpolation through the knots, held after the last knot (R1).
+double pwl_at(const std::vector<double>& kt, const std::vector<double>& kc, double t) {
+  if (t >= kt.back()) return kc.back();
+  size_t k = size_t(std::upper_bound(kt.begin(), kt.end(), t) - kt.begin()) - 1;  // kt[k] <= t < kt[k+1]
+  double a = (t - kt[k]) / (kt[k + 1] - kt[k]);
+  return kc[k] + (kc[k + 1] - kc[k]) * a;
+}
+
+// sorted, de-duplicated union of {0}, `extra` (<= tend), frame starts and ends
+std::vector<double> make_grid(const abc_ctx* c, const std::vector<double>& extra) {
+  double tend = c->fs[c->L - 1] + c->fd[c->L - 1];
+  std::vector<double> t;
+  t.reserve(extra.size() + 2 * c->L + 1);
+  t.push_back(0.0);
+  for (double x : extra)
+    if (x <= tend) t.push_back(x);
+  for (uint32_t f = 0; f < c->L; ++f) {
+    t.push_back(c->fs[f]);
+    t.push_back(c->fs[f] + c->fd[f]);
+  }
+  std::sort(t.begin(), t.end());
+  t.erase(std::unique(t.begin(), t.end()), t.end());
+  return t;
+}
+
+std::vector<int> segment_frames(const abc_ctx* c, const std::vector<double>& t) {
+  std::vector<int> sf(t.size() > 1 ? t.size() - 1 : 1, -1);
+  uint32_t f = 0;
+  for (size_t k = 0; k + 1 < t.size(); ++k) {
+    while (f < c->L && t[k] >= c->fs[f] + c->fd[f]) ++f;
+    if (f < c->L && t[k] >= c->fs[f] && t[k + 1] <= c->fs[f] + c->fd[f]) sf[k] = int(f);
+  }
+  return sf;
+}
+
+// int_ts^te of the Feng curve, closed form
+double feng_frame_integral(const double* b, double ts, double te) {
+  auto G = [](double x, double a, double z) {  // int_a^z e^{-x t} dt
+    double d = z - a;
+    double ph = (x * d == 0.0) ? 1.0 : -std::expm1(-x * d) / (x * d);
+    return std::exp(-x * a) * d * ph;
+  };
+  double k1 = b[3];
+  double tint = (ts * std::exp(-k1 * ts) - te * std::exp(-k1 * te)) / k1 + G(k1, ts, te) / k1;
+  return b[0] * tint - (b[1] + b[2]) * G(k1, ts, te) + b[1] * G(b[4], ts, te) + b[2] * G(b[5], ts, te);
+}
+
+abc_status build_tables(abc_ctx* ctx) {
+  if (!ctx->dirty) return ABC_OK;
+  const uint32_t L = ctx->L;
+  std::vector<double> fe(L), favg(L, 0.0);
+  for (uint32_t f = 0; f < L; ++f) fe[f] = ctx->fs[f] + ctx->fd[f];
+  std::vector<double> gt{0.0, 1.0}, gc{0.0, 0.0}, ft{0.0, 1.0}, fc{0.0, 0.0};
+  std::vector<int> gfr{-1}, ffr{-1};
+  if (ctx->input_kind == ABC_INPUT_PWL) {
+    gt = make_grid(ctx, ctx->kt);
+    gc.resize(gt.size());
+    for (size_t k = 0; k < gt.size(); ++k) gc[k] = pwl_at(ctx->kt, ctx->kc, gt[k]);
+    gfr = segment_frames(ctx, gt);
+    for (size_t k = 0; k + 1 < gt.size(); ++k)
+      if (gfr[k] >= 0) favg[gfr[k]] += 0.5 * (gt[k + 1] - gt[k]) * (gc[k] + gc[k + 1]);
+    bool lpnt = false;
+    for (uint32_t m = 0; m < ctx->M; ++m) lpnt |= ctx->cfg.model[m].kind == ABC_LPNTPET;
+    if (lpnt) {
+      double delta = ctx->cfg.lpnt_step_min > 0.0 ? ctx->cfg.lpnt_step_min : 0.05;
+      double tend = fe[L - 1];
+      std::vector<double> extra;
+      for (uint64_t k = 0; double(k) * delta < tend; ++k) extra.push_back(double(k) * delta);
+      for (double x : ctx->kt) extra.push_back(x);
+      ft = make_grid(ctx, extra);
+      if (ft.size() > 4000000) return fail(ctx, ABC_E_UNSUPPORTED, "lp-ntPET grid too fine");
+      fc.resize(ft.size());
+      for (size_t k = 0; k < ft.size(); ++k) fc[k] = pwl_at(ctx->kt, ctx->kc, ft[k]);
+      ffr = segment_frames(ctx, ft);
+    }
+  } else {
+    for (uint32_t f = 0; f < L; ++f) favg[f] = feng_frame_integral(ctx->feng, ctx->fs[f], fe[f]);
+  }
+  std::vector<float> wsc(L);
+  for (uint32_t f = 0; f < L; ++f) {
+    if (ctx->unit_w) wsc[f] = 1.0f;
+    else if (ctx->cfg.distance == ABC_DIST_WL2) wsc[f] = float(std::sqrt(double(ctx->w[f])));
+    else wsc[f] = ctx->w[f];
+  }
+  CK(upload(ctx->d_fdur, ctx->fd));
+  CK(upload(ctx->d_fs, ctx->fs));
+  CK(upload(ctx->d_fe, fe));
+  CK(upload(ctx->d_favg, favg));
+  CK(upload(ctx->d_w, ctx->w));
+  CK(upload(ctx->d_wsc, wsc));
+  CK(upload(ctx->d_gt, gt));
+  CK(upload(ctx->d_gc, gc));
+  CK(upload(ctx->d_gframe, gfr));
+  CK(upload(ctx->d_ft, ft));
+  CK(upload(ctx->d_fc, fc));
+  CK(upload(ctx->d_fframe, ffr));
+  ctx->G = uint32_t(gt.size());
+  ctx->GF = uint32_t(ft.size());
+  ctx->dirty = false;
+  return ABC_OK;
+}
+
+Tables make_tables(const abc_ctx* c, uint32_t LS) {
+  Tables T{};
+  T.L = c->L;
+  T.LS = LS;
+  T.fdur = c->d_fdur.as<double>();
+  T.fs = c->d_fs.as<double>();
+  T.fe = c->d_fe.as<double>();
+  T.favg_in = c->d_favg.as<double>();
+  T.w = c->d_w.as<float>();
+  T.G = c->G;
+  T.gt = c->d_gt.as<double>();
+  T.gc = c->d_gc.as<double>();
+  T.gframe = c->d_gframe.as<int>();
+  T.GF = c->GF;
+  T.ft = c->d_ft.as<double>();
+  T.fc = c->d_fc.as<double>();
+  T.fframe = c->d_fframe.as<int>();
+  T.feng = c->input_kind == ABC_INPUT_FENG;
+  for (int k = 0; k < 6; ++k) T.fb[k] = c->feng[k];
+  return T;
+}
+
+// Rigorous |D32 - D| bound of the FP32 pass, doubled for margin.
+ErrBound error_bound(const abc_ctx* c, uint32_t LP) {
+  const double u = std::ldexp(1.0, -24);
+  const double g = LP * u / (1.0 - LP * u);
+  ErrBound e{0, 0, 0, 0};
+  if (c->cfg.distance == ABC_DIST_WL2) {
+    if (c->unit_w) {
+      e.a = 2.0 * (g + 3.0 * u);
+    } else {
+      e.a = 2.0 * (g + 6.1 * u);
+      e.b = 2.0 * 4.1 * u;
+      e.c = 2.0 * 16.5 * u * u;
+    }
+  } else {
+    if (c->unit_w) {
+      e.a = 2.0 * (g + 2.0 * u);
+    } else {
+      e.a = 2.0 * (g + 3.1 * u);
+      e.d = 2.0 * 2.1 * u;
+    }
+  }
+  return e;
+}
+
+__global__ void finite_check_kernel(const float* x, uint64_t n, int* flag) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x)
+    if (!isfinite(x[e])) *flag = 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t abc_abi_version(void) { return VPETABC_ABI_VERSION; }
+
+abc_status abc_init(const abc_config* cfg, abc_ctx** out) {
+  if (!out) return ABC_E_ARG;
+  *out = nullptr;
+  if (!cfg || cfg->struct_size != sizeof(abc_config)) return ABC_E_ARG;
+  if (cfg->n_models < 1 || cfg->n_models > ABC_MAX_MODELS) return ABC_E_ARG;
+  if (cfg->reserved1 != 0) return ABC_E_ARG;
+  uint64_t N = 0;
+  int fam = -1;
+  for (uint32_t m = 0; m < cfg->n_models; ++m) {
+    const abc_model_spec& ms = cfg->model[m];
+    if (ms.kind < ABC_2TCM_IRR || ms.kind > ABC_LPNTPET || ms.reserved0 != 0 || ms.n_draws == 0) return ABC_E_ARG;
+    int f = ms.kind >= ABC_MRTM;
+    if (fam >= 0 && f != fam) return ABC_E_ARG;
+    fam = f;
+    for (uint32_t k = 0; k < family_width(ms.kind); ++k)
+      if (!std::isfinite(ms.lo[k]) || !std::isfinite(ms.hi[k]) || !(ms.lo[k] <= ms.hi[k])) return ABC_E_ARG;
+    if (ms.kind <= ABC_2TCM_REV && !(ms.lo[2] > 0.0f)) return ABC_E_ARG;  // r > 0 (R3)
+    if (ms.kind == ABC_LPNTPET && !(ms.lo[5] > 0.0f)) return ABC_E_ARG;   // tP > tD
+    N += ms.n_draws;
+  }
+  if (N >= (1ull << 32)) return ABC_E_ARG;
+  if (cfg->distance != ABC_DIST_L1 && cfg->distance != ABC_DIST_WL2) return ABC_E_ARG;
+  if (cfg->accept == ABC_ACCEPT_TOPN) {
+    if (cfg->n_accept == 0 || cfg->n_accept > N || cfg->n_accept > 4096) return ABC_E_ARG;
+  } else if (cfg->accept == ABC_ACCEPT_EPS) {
+    if (!(cfg->epsilon >= 0.0)) return ABC_E_ARG;
+  } else {
+    return ABC_E_ARG;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) return ABC_E_CUDA;
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return ABC_E_CUDA;
+  abc_ctx* c = new (std::nothrow) abc_ctx();
+  if (!c) return ABC_E_NOMEM;
+  c->cfg = *cfg;
+  c->dev = cfg->device;
+  c->N = N;
+  c->M = cfg->n_models;
+  c->P = family_width(cfg->model[0].kind);
+  c->prior.M = c->M;
+  c->prior.seed_lo = uint32_t(cfg->seed);
+  c->prior.seed_hi = uint32_t(cfg->seed >> 32);
+  uint64_t off = 0;
+  for (uint32_t m = 0; m < c->M; ++m) {
+    ModelDev& md = c->prior.m[m];
+    const abc_model_spec& ms = cfg->model[m];
+    md.kind = ms.kind;
+    md.P = family_width(ms.kind);
+    md.begin = off;
+    off += ms.n_draws;
+    md.end = off;
+    for (int k = 0; k < ABC_MAX_P; ++k) {
+      md.lo[k] = ms.lo[k];
+      md.span[k] = ms.hi[k] - ms.lo[k];  // FP32 subtraction (theta = fmaf(span, u, lo))
+    }
+  }
+  for (uint32_t m = c->M; m < ABC_MAX_MODELS; ++m) c->prior.m[m].begin = ~0ull;
+  if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return ABC_E_CUDA;
+  }
+  c->stream = c->own;
+  c->ev_ok = true;
+  for (int k = 0; k < EV_N; ++k)
+    if (cudaEventCreate(&c->ev[k]) != cudaSuccess) c->ev_ok = false;
+  c->stats.struct_size = sizeof(abc_stats);
+  *out = c;
+  return ABC_OK;
+}
+
+abc_status abc_set_input_function(abc_ctx* ctx, int32_t kind, const double* t, const double* v, uint32_t n) {
+  if (!ctx) return ABC_E_ARG;
+  if (kind == ABC_INPUT_FENG) {
+    if (!v || n != 6) return fail(ctx, ABC_E_ARG, "FENG input needs value[6]");
+    for (int k = 0; k < 6; ++k)
+      if (!std::isfinite(v[k])) return fail(ctx, ABC_E_ARG, "non-finite Feng parameter");
+    if (!(v[3] > 0 && v[4] > 0 && v[5] > 0)) return fail(ctx, ABC_E_ARG, "Feng rates must be > 0");
+    if (ctx->cfg.model[0].kind >= ABC_MRTM) return fail(ctx, ABC_E_UNSUPPORTED, "reference models need a PWL C_r");
+    std::memcpy(ctx->feng, v, sizeof ctx->feng);
+  } else if (kind == ABC_INPUT_PWL) {
+    if (!t || !v || n < 1) return fail(ctx, ABC_E_ARG, "PWL input needs knots");
+    if (t[0] != 0.0) return fail(ctx, ABC_E_ARG, "first knot must be at t = 0");
+    for (uint32_t k = 0; k < n; ++k) {
+      if (!std::isfinite(t[k]) || !std::isfinite(v[k])) return fail(ctx, ABC_E_ARG, "non-finite knot");
+      if (k > 0 && !(t[k] > t[k - 1])) return fail(ctx, ABC_E_ARG, "knot times must increase");
+    }
+    ctx->kt.assign(t, t + n);
+    ctx->kc.assign(v, v + n);
+  } else {
+    return fail(ctx, ABC_E_ARG, "unknown input kind");
+  }
+  ctx->input_kind = kind;
+  ctx->have_input = true;
+  ctx->dirty = true;
+  return ABC_OK;
+}
+
+abc_status abc_set_frames(abc_ctx* ctx, const double* st, const double* du, const float* wt, uint32_t L) {
+  if (!ctx) return ABC_E_ARG;
+  if (!st || !du || L < 1 || L > ABC_MAX_L) return fail(ctx, ABC_E_ARG, "need 1..128 frames");
+  for (uint32_t f = 0; f < L; ++f) {
+    if (!std::isfinite(st[f]) || !std::isfinite(du[f]) || !(du[f] > 0.0) || st[f] < 0.0)
+      return fail(ctx, ABC_E_ARG, "frame durations must be > 0 and starts >= 0");
+    if (f > 0 && st[f] < st[f - 1] + du[f - 1]) return fail(ctx, ABC_E_ARG, "frames overlap or are not increasing");
+    if (wt && !(wt[f] > 0.0f && std::isfinite(wt[f]))) return fail(ctx, ABC_E_ARG, "weights must be finite and > 0");
+  }
+  ctx->fs.assign(st, st + L);
+  ctx->fd.assign(du, du + L);
+  ctx->w.assign(L, 1.0f);
+  ctx->unit_w = true;
+  if (wt) {
+    for (uint32_t f = 0; f < L; ++f) {
+      ctx->w[f] = wt[f];
+      if (wt[f] != 1.0f) ctx->unit_w = false;
+    }
+  }
+  ctx->L = L;
+  ctx->have_frames = true;
+  ctx->dirty = true;
+  return ABC_OK;
+}
+
+abc_status abc_set_stream(abc_ctx* ctx, void* s) {
+  if (!ctx) return ABC_E_ARG;
+  ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+  return ABC_OK;
+}
+
+abc_status abc_sync(abc_ctx* ctx) {
+  if (!ctx) return ABC_E_ARG;
+  CK(cudaSetDevice(ctx->dev));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return ABC_OK;
+}
+
+abc_status abc_get_stats(const abc_ctx* ctx, abc_stats* s) {
+  if (!ctx || !s || s->struct_size != sizeof(abc_stats)) return ABC_E_ARG;
+  *s = ctx->stats;
+  return ABC_OK;
+}
+
+abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t ptr_flags, abc_result* out) {
+  if (!ctx || !out) return ABC_E_ARG;
+  if (!ctx->have_input || !ctx->have_frames) return fail(ctx, ABC_E_STATE, "input function and frames must be set");
+  if (ptr_flags & ~(ABC_PTR_TACS_DEVICE | ABC_PTR_OUT_DEVICE)) return fail(ctx, ABC_E_ARG, "unknown ptr_flags");
+  if (ctx->cfg.model[0].kind >= ABC_MRTM && ctx->input_kind != ABC_INPUT_PWL)
+    return fail(ctx, ABC_E_UNSUPPORTED, "reference models need a PWL C_r");
+  if (J >= (1ull << 32)) return fail(ctx, ABC_E_ARG, "J must be < 2^32");
+  abc_stats& S = ctx->stats;
+  std::memset(&S, 0, sizeof S);
+  S.struct_size = sizeof(abc_stats);
+  S.n_voxels = J;
+  S.n_draws = ctx->N;
+  if (J == 0) return ABC_OK;
+  if (!tacs) return fail(ctx, ABC_E_ARG, "tacs is NULL");
+  CK(cudaSetDevice(ctx->dev));
+  abc_status bs = build_tables(ctx);
+  if (bs != ABC_OK) return bs;
+
+  const cudaStream_t st = ctx->stream;
+  const uint64_t N = ctx->N;
+  const uint32_t L = ctx->L, LS = (L + 3) & ~3u, M = ctx->M, P = ctx->P;
+  const uint32_t LP = scan_lp_for(L);
+  const bool eps = ctx->cfg.accept == ABC_ACCEPT_EPS;
+  const bool exact = (ctx->cfg.flags & ABC_FLAG_EXACT) && !eps;
+  const bool timing = (ctx->cfg.flags & ABC_FLAG_TIMING) && ctx->ev_ok;
+  const bool count_work = (ctx->cfg.flags & ABC_FLAG_COUNT_WORK) != 0;
+  const uint32_t n = ctx->cfg.n_accept;
+  uint32_t K = 0;
+  if (!eps) {
+    uint64_t k = uint64_t(n) + std::max<uint64_t>(8, n / 16);
+    k = (k + 7) & ~7ull;
+    K = uint32_t(std::min<uint64_t>(k, N));
+  }
+  S.lp = LP;
+  S.heap_k = K;
+
+  // ---- memory plan (checked before allocating) ----
+  const bool host_tacs = !(ptr_flags & ABC_PTR_TACS_DEVICE);
+  const bool host_out = !(ptr_flags & ABC_PTR_OUT_DEVICE);
+  struct OutDesc {
+    void* user;
+    size_t bytes;
+  };
+  OutDesc od[11] = {
+      {out->prob, 4 * J * M},       {out->preferred, 4 * J},      {out->count, 4 * J * M},
+      {out->mean, 4 * J * P},       {out->sd, 4 * J * P},         {out->q, 12 * J * P},
+      {out->ki_mean, 4 * J},        {out->ki_sd, 4 * J},          {out->ki_q, 12 * J},
+      {eps ? nullptr : out->acc_idx, 8 * J * n}, {eps ? nullptr : out->acc_dist, 8 * J * n}};
+  size_t out_bytes = 0;
+  for (auto& d : od)
+    if (d.user && host_out) out_bytes += (d.bytes + 255) & ~size_t(255);
+  size_t need = 0;
+  need += sizeof(float) * N * LS;                        // exact bank
+  if (!exact) need += sizeof(float) * N * LP;            // scan bank
+  if (!eps) need += size_t(8) * J * K + 4 * J;           // heaps
+  need += size_t(12) * J * (n ? n : 1);                  // exact heaps (fallback)
+  if (eps) need += sizeof(double) * J * M * MOMW;
+  if (host_tacs) need += sizeof(float) * J * L;
+  need += out_bytes + 8 * J + (64u << 20);
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  size_t have = free_b + ctx->bank.cap + ctx->bankp.cap + ctx->heap.cap + ctx->hd.cap + ctx->hidx.cap + ctx->tacs.cap +
+                ctx->outs.cap + ctx->mom.cap;
+  if (need > have) return fail(ctx, ABC_E_NOMEM, "device memory: need " + std::to_string(need >> 20) + " MiB");
+
+  CK(ctx->bank.ensure(sizeof(float) * N * LS));
+  if (!exact) CK(ctx->bankp.ensure(sizeof(float) * N * LP));
+  CK(ctx->var.ensure(sizeof(double) * kMaxLP));
+  CK(ctx->perm.ensure(sizeof(int) * kMaxLP));
+  CK(ctx->wsp.ensure(sizeof(float) * kMaxLP));
+  if (!eps) {
+    CK(ctx->heap.ensure(size_t(8) * J * std::max<uint32_t>(K, 1)));
+    CK(ctx->heap_cnt.ensure(4 * J));
+    CK(ctx->hd.ensure(sizeof(double) * J * n));
+    CK(ctx->hidx.ensure(sizeof(uint32_t) * J * n));
+  } else {
+    CK(ctx->mom.ensure(sizeof(double) * J * M * MOMW));
+  }
+  CK(ctx->d_prior.ensure(sizeof(PriorDev)));
+  CK(cudaMemcpyAsync(ctx->d_prior.p, &ctx->prior, sizeof(PriorDev), cudaMemcpyHostToDevice, st));
+  CK(ctx->fb_list.ensure(4 * J));
+  CK(ctx->fb_len.ensure(16));
+  CK(ctx->work.ensure(16));
+  CK(ctx->flag.ensure(16));
+  if (host_tacs) CK(ctx->tacs.ensure(sizeof(float) * J * L));
+  if (out_bytes) CK(ctx->outs.ensure(out_bytes));
+
+  // device-side result pointers
+  abc_result dout = *out;
+  if (eps) {
+    dout.acc_idx = nullptr;
+    dout.acc_dist = nullptr;
+  }
+  if (host_out) {
+    char* base = ctx->outs.as<char>();
+    void** fields[11] = {(void**)&dout.prob,    (void**)&dout.preferred, (void**)&dout.count,
+                         (void**)&dout.mean,    (void**)&dout.sd,        (void**)&dout.q,
+                         (void**)&dout.ki_mean, (void**)&dout.ki_sd,     (void**)&dout.ki_q,
+                         (void**)&dout.acc_idx, (void**)&dout.acc_dist};
+    size_t off = 0;
+    for (int k = 0; k < 11; ++k) {
+      if (od[k].user) {
+        *fields[k] = base + off;
+        off += (od[k].bytes + 255) & ~size_t(255);
+      } else {
+        *fields[k] = nullptr;
+      }
+    }
+  }
+
+  uint32_t launches = 0;
+  auto rec = [&](int k) {
+    if (timing) cudaEventRecord(ctx->ev[k], st);
+  };
+  rec(EV_START);
+  const float* d_tacs = tacs;
+  if (host_tacs) {
+    CK(cudaMemcpyAsync(ctx->tacs.p, tacs, sizeof(float) * J * L, cudaMemcpyHostToDevice, st));
+    d_tacs = ctx->tacs.as<float>();
+  }
+  rec(EV_H2D);
+  CK(cudaMemsetAsync(ctx->flag.p, 0, 16, st));
+  CK(cudaMemsetAsync(ctx->fb_len.p, 0, 16, st));
+  CK(cudaMemsetAsync(ctx->work.p, 0, 16, st));
+  finite_check_kernel<<<148, 256, 0, st>>>(d_tacs, J * L, ctx->flag.as<int>());
+  ++launches;
+
+  // K1: bank
+  BankParams bp{make_tables(ctx, LS), N, ctx->bank.as<float>()};
+  launch_bank(bp, ctx->prior, st);
+  ++launches;
+  ctx->bank_valid = true;
+  ctx->bank_L = L;
+  rec(EV_BANK);
+
+  const ErrBound eb = error_bound(ctx, LP);
+  if (!exact) {
+    OrderParams op{};
+    op.bank = ctx->bank.as<float>();
+    op.N = N;
+    op.L = L;
+    op.LS = LS;
+    op.LP = LP;
+    op.wsc = ctx->d_wsc.as<float>();
+    op.var = ctx->var.as<double>();
+    op.perm = ctx->perm.as<int>();
+    op.wsp = ctx->wsp.as<float>();
+    op.bankp = ctx->bankp.as<float>();
+    op.reorder = !(ctx->cfg.flags & ABC_FLAG_NO_REORDER);
+    launch_order(op, st);
+    launches += 3;
+  }
+  rec(EV_ORDER);
+
+  if (!exact) {
+    ScanParams sp{};
+    sp.bankp = ctx->bankp.as<float>();
+    sp.N = N;
+    sp.tacs = d_tacs;
+    sp.J = J;
+    sp.L = L;
+    sp.perm = ctx->perm.as<int>();
+    sp.wsp = ctx->wsp.as<float>();
+    sp.K = K;
+    sp.heap = ctx->heap.as<unsigned long long>();
+    sp.heap_cnt = ctx->heap_cnt.as<uint32_t>();
+    sp.prune = !(ctx->cfg.flags & ABC_FLAG_NO_PRUNE);
+    sp.work = ctx->work.as<unsigned long long>();
+    sp.eps_mode = eps;
+    sp.eps = ctx->cfg.epsilon;
+    sp.w = ctx->d_w.as<float>();
+    sp.bank = ctx->bank.as<float>();
+    sp.LS = LS;
+    sp.dist = ctx->cfg.distance;
+    sp.unit_w = ctx->unit_w;
+    sp.mom = eps ? ctx->mom.as<double>() : nullptr;
+    sp.eb = eb;
+    sp.prior_g = ctx->d_prior.as<PriorDev>();
+    sp.M = M;
+    if (eps) CK(cudaMemsetAsync(ctx->mom.p, 0, sizeof(double) * J * M * MOMW, st));
+    CK(launch_scan(sp, LP, count_work, st));
+    ++launches;
+  }
+  rec(EV_SCAN);
+
+  ReduceParams rp{};
+  rp.K = K;
+  rp.heap = ctx->heap.as<unsigned long long>();
+  rp.heap_cnt = ctx->heap_cnt.as<uint32_t>();
+  rp.hd = ctx->hd.as<double>();
+  rp.hidx = ctx->hidx.as<uint32_t>();
+  rp.J = J;
+  rp.n = n;
+  rp.bank = ctx->bank.as<float>();
+  rp.N = N;
+  rp.L = L;
+  rp.LS = LS;
+  rp.LP = LP;
+  rp.tacs = d_tacs;
+  rp.w = ctx->d_w.as<float>();
+  rp.dist = ctx->cfg.distance;
+  rp.unit_w = ctx->unit_w;
+  rp.eb = eb;
+  rp.prior = ctx->prior;
+  rp.P = P;
+  rp.fb_list = ctx->fb_list.as<uint32_t>();
+  rp.fb_len = ctx->fb_len.as<uint32_t>();
+  rp.out = dout;
+
+  ExactParams xp{};
+  xp.bank = ctx->bank.as<float>();
+  xp.N = N;
+  xp.L = L;
+  xp.LS = LS;
+  xp.tacs = d_tacs;
+  xp.w = ctx->d_w.as<float>();
+  xp.dist = ctx->cfg.distance;
+  xp.n = n;
+  xp.J = J;
+  xp.hd = ctx->hd.as<double>();
+  xp.hi = ctx->hidx.as<uint32_t>();
+
+  if (eps) {
+    EpsReduceParams ep{ctx->mom.as<double>(), J, ctx->prior, P, dout};
+    launch_eps_reduce(ep, st);
+    ++launches;
+    rec(EV_CERT);
+    rec(EV_FB);
+  } else if (exact) {
+    launch_exact_scan(xp, st);
+    rp.exact = 1;
+    rp.list = nullptr;
+    rp.list_len = nullptr;
+    rec(EV_CERT);
+    launch_certify_reduce(rp, st);
+    launches += 2;
+    rec(EV_FB);
+  } else {
+    rp.exact = 0;
+    rp.list = nullptr;
+    rp.list_len = nullptr;
+    launch_certify_reduce(rp, st);
+    ++launches;
+    rec(EV_CERT);
+    // uncertified voxels: exact scan + reduce over the device-side list (no host sync)
+    xp.list = ctx->fb_list.as<uint32_t>();
+    xp.list_len = ctx->fb_len.as<uint32_t>();
+    launch_exact_scan(xp, st);
+    ReduceParams rx = rp;
+    rx.exact = 1;
+    rx.list = xp.list;
+    rx.list_len = xp.list_len;
+    rx.fb_list = nullptr;
+    launch_certify_reduce(rx, st);
+    launches += 2;
+    rec(EV_FB);
+  }
+  CK(cudaGetLastError());
+  if (host_out) {
+    void* srcs[11] = {dout.prob, dout.preferred, dout.count, dout.mean, dout.sd, dout.q,
+                      dout.ki_mean, dout.ki_sd, dout.ki_q, dout.acc_idx, dout.acc_dist};
+    for (int k = 0; k < 11; ++k)
+      if (od[k].user && srcs[k]) CK(cudaMemcpyAsync(od[k].user, srcs[k], od[k].bytes, cudaMemcpyDeviceToHost, st));
+  }
+  rec(EV_D2H);
+  int h_flag = 0;
+  uint32_t h_fb = 0;
+  unsigned long long h_work = 0;
+  CK(cudaMemcpyAsync(&h_flag, ctx->flag.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h_fb, ctx->fb_len.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h_work, ctx->work.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  S.gpu_launches = launches;
+  S.n_fallback = h_fb;
+  S.frame_updates = h_work;
+  if (timing) {
+    auto ms = [&](int a, int b) {
+      float x = 0.0f;
+      cudaEventElapsedTime(&x, ctx->ev[a], ctx->ev[b]);
+      return double(x);
+    };
+    S.ms_h2d = ms(EV_START, EV_H2D);
+    S.ms_bank = ms(EV_H2D, EV_BANK);
+    S.ms_order = ms(EV_BANK, EV_ORDER);
+    S.ms_scan = ms(EV_ORDER, EV_SCAN);
+    S.ms_certify = ms(EV_SCAN, EV_CERT);
+    S.ms_fallback = ms(EV_CERT, EV_FB);
+    S.ms_d2h = ms(EV_FB, EV_D2H);
+    S.ms_total = ms(EV_START, EV_D2H);
+  }
+  if (h_flag) return fail(ctx, ABC_E_ARG, "non-finite TAC value");
+  return ABC_OK;
+}
+
+abc_status abc_model_select(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t ptr_flags, float* prob,
+                            int32_t* preferred) {
+  abc_result r;
+  std::memset(&r, 0, sizeof r);
+  r.prob = prob;
+  r.preferred = preferred;
+  return abc_run_voxels(ctx, tacs, J, ptr_flags, &r);
+}
+
+abc_status abc_get_bank(const abc_ctx* ctx_c, float* out, uint64_t first, uint64_t count) {
+  abc_ctx* ctx = const_cast<abc_ctx*>(ctx_c);
+  if (!ctx || !out) return ABC_E_ARG;
+  if (!ctx->bank_valid) return fail(ctx, ABC_E_STATE, "no bank: run first");
+  if (first > ctx->N || count > ctx->N - first) return fail(ctx, ABC_E_ARG, "bank rows out of range");
+  CK(cudaSetDevice(ctx->dev));
+  const uint32_t LS = (ctx->bank_L + 3) & ~3u;
+  CK(cudaMemcpy2D(out, sizeof(float) * ctx->bank_L, ctx->bank.as<float>() + first * LS, sizeof(float) * LS,
+                  sizeof(float) * ctx->bank_L, count, cudaMemcpyDeviceToHost));
+  return ABC_OK;
+}
+
+const char* abc_last_error(const abc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void abc_destroy(abc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->dev);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
+                    &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,
+                    &ctx->bank,   &ctx->bankp, &ctx->var,    &ctx->perm,   &ctx->wsp,        &ctx->heap,
+                    &ctx->heap_cnt, &ctx->tacs, &ctx->fb_list, &ctx->fb_len, &ctx->work,     &ctx->hd,
+                    &ctx->hidx,   &ctx->mom,   &ctx->flag,   &ctx->outs};
+  for (DevBuf* b : bufs) b->release();
+  for (int k = 0; k < EV_N; ++k)
+    if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+}  // extern "C"

@@ -1,0 +1,279 @@
+// bank.cu -- K1: simulation bank (Alg. 1 lines 1-3) and K1b/c: frame ordering and
+// the negated, prescaled scan-order copy used by the FP32 pass.
+//
+// Each thread simulates one draw in FP64 and stores the frame averages rounded to FP32
+// (the method's FP32 TAC):
+//   2TCM (eq:2TCM P:69-74, eq:2TCM_op P:75-80, C_wb = C_p P:80):
+//     h(t) = c1 e^{-a1 t} + c2 e^{-a2 t},  a2 = (s+r)/2, a1 = 2 k2 k4/(s+r),
+//     s = k2+k3+k4, r^2 = (k2-k4)^2 + k3 (k3 + 2 (k2+k4)),
+//     c1 = K1 (k3+k4-a1)/(a2-a1), c2 = K1 (a2-k3-k4)/(a2-a1),
+//     value_f = [(1-Vb)(c1 S_f(a1) + c2 S_f(a2)) + Vb int_f C_p] / dt_f,
+//     S_f(a) = int_f (C_p (x) e^{-a.}) dt: exact recurrences on the PWL grid, or the Feng
+//     closed form.
+//   MRTM (eq:lp-ntPET with gamma = 0): value_f = [R1 int_f C_r + (k2 - R1 k2a) S_f(k2a)]/dt_f.
+//   lp-ntPET (eq:lp-ntPET, eq:Bt): z = C_t - R1 C_r, z' = (k2 - R1 a) C_r - a z,
+//     a(t) = k2a + gamma g(t) frozen at each substep midpoint (R4).
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace vpet {
+
+namespace {
+
+struct FrameAcc {
+  int cur = -1;
+  double A = 0.0, B = 0.0;
+};
+
+// ---- piecewise-linear input on a grid: both rates of the 2TCM at once ----
+__device__ void sim_2tcm_pwl(const Tables& T, double a1, double a2, double c1, double c2, double Vb,
+                             float* out) {
+  double I1 = 0.0, I2 = 0.0;
+  FrameAcc fa;
+  auto flush = [&](int f) {
+    double v = ((1.0 - Vb) * (c1 * fa.A + c2 * fa.B) + Vb * T.favg_in[f]) / T.fdur[f];
+    out[f] = __double2float_rn(v);
+  };
+  for (uint32_t k = 0; k + 1 < T.G; ++k) {
+    double t0 = T.gt[k], t1 = T.gt[k + 1];
+    double h = t1 - t0;
+    double ck = T.gc[k], ck1 = T.gc[k + 1];
+    int f = T.gframe[k];
+    Phi p = phi_all(a1 * h);
+    Phi q = phi_all(a2 * h);
+    double dc = ck1 - ck;
+    double s1 = h * p.p1 * I1 + h * h * (ck1 * p.ps - dc * p.om);
+    double s2 = h * q.p1 * I2 + h * h * (ck1 * q.ps - dc * q.om);
+    if (f != fa.cur) {
+      if (fa.cur >= 0) flush(fa.cur);
+      fa.cur = f;
+      fa.A = 0.0;
+      fa.B = 0.0;
+    }
+    fa.A += s1;
+    fa.B += s2;
+    I1 = p.e * I1 + h * (ck * p.ch + ck1 * p.ps);
+    I2 = q.e * I2 + h * (ck * q.ch + ck1 * q.ps);
+  }
+  if (fa.cur >= 0) flush(fa.cur);
+}
+
+// ---- Feng input: closed forms of e^{-a t} (x) {e^{-k t}, t e^{-k t}} and their integrals ----
+__device__ inline double convE(double a, double k, double t) {
+  double mn = fmin(a, k);
+  return t * exp(-mn * t) * phi1_only(fabs(a - k) * t);
+}
+__device__ inline double convEt(double a, double k, double t) {
+  if (a >= k) {
+    Phi p = phi_all((a - k) * t);
+    return t * t * exp(-k * t) * p.ps;
+  }
+  Phi p = phi_all((k - a) * t);
+  return t * t * exp(-a * t) * p.ch;
+}
+__device__ inline double Gexp(double x, double ts, double te) {
+  double d = te - ts;
+  return exp(-x * ts) * d * phi1_only(x * d);
+}
+// int_ts^te E dt via E' = e^{-k t} - a E = e^{-a t} - k E (divide by the larger rate)
+__device__ inline double intE(double a, double k, double ts, double te) {
+  double dE = convE(a, k, te) - convE(a, k, ts);
+  return (a >= k) ? (Gexp(k, ts, te) - dE) / a : (Gexp(a, ts, te) - dE) / k;
+}
+// int Et via Et' = E - k Et
+__device__ inline double intEt(double a, double k, double ts, double te) {
+  double dEt = convEt(a, k, te) - convEt(a, k, ts);
+  return (intE(a, k, ts, te) - dEt) / k;
+}
+__device__ inline double feng_conv(const double* b, double a, double ts, double te) {
+  return b[0] * intEt(a, b[3], ts, te) - (b[1] + b[2]) * intE(a, b[3], ts, te) + b[1] * intE(a, b[4], ts, te) +
+         b[2] * intE(a, b[5], ts, te);
+}
+
+__device__ void sim_2tcm_feng(const Tables& T, double a1, double a2, double c1, double c2, double Vb, float* out) {
+  for (uint32_t f = 0; f < T.L; ++f) {
+    double ts = T.fs[f], te = T.fe[f];
+    double S1 = feng_conv(T.fb, a1, ts, te);
+    double S2 = feng_conv(T.fb, a2, ts, te);
+    double v = ((1.0 - Vb) * (c1 * S1 + c2 * S2) + Vb * T.favg_in[f]) / T.fdur[f];
+    out[f] = __double2float_rn(v);
+  }
+}
+
+__device__ void sim_mrtm(const Tables& T, double R1, double k2, double k2a, float* out) {
+  double I = 0.0;
+  FrameAcc fa;
+  double kf = k2 - R1 * k2a;
+  auto flush = [&](int f) { out[f] = __double2float_rn((R1 * T.favg_in[f] + kf * fa.A) / T.fdur[f]); };
+  for (uint32_t k = 0; k + 1 < T.G; ++k) {
+    double h = T.gt[k + 1] - T.gt[k];
+    double ck = T.gc[k], ck1 = T.gc[k + 1];
+    int f = T.gframe[k];
+    Phi p = phi_all(k2a * h);
+    double s = h * p.p1 * I + h * h * (ck1 * p.ps - (ck1 - ck) * p.om);
+    if (f != fa.cur) {
+      if (fa.cur >= 0) flush(fa.cur);
+      fa.cur = f;
+      fa.A = 0.0;
+    }
+    fa.A += s;
+    I = p.e * I + h * (ck * p.ch + ck1 * p.ps);
+  }
+  if (fa.cur >= 0) flush(fa.cur);
+}
+
+__device__ void sim_lpntpet(const Tables& T, const float* th, float* out) {
+  double R1 = th[0], k2 = th[1], k2a = th[2], gam = th[3], tD = th[4], tP = th[5], al = th[6];
+  double inv = 1.0 / (tP - tD);
+  double z = 0.0;
+  FrameAcc fa;
+  auto flush = [&](int f) { out[f] = __double2float_rn((fa.A + R1 * T.favg_in[f]) / T.fdur[f]); };
+  for (uint32_t k = 0; k + 1 < T.GF; ++k) {
+    double t0 = T.ft[k], t1 = T.ft[k + 1];
+    double h = t1 - t0;
+    double tm = 0.5 * (t0 + t1);
+    double g = 0.0;
+    if (tm > tD) {
+      double x = (tm - tD) * inv;
+      g = exp(al * (log(x) + 1.0 - x));  // x^alpha e^{alpha (1-x)}
+    }
+    double ab = k2a + gam * g;
+    Phi p = phi_all(ab * h);
+    double kf = k2 - R1 * ab;
+    double fk = kf * T.fc[k], fk1 = kf * T.fc[k + 1];
+    double s = h * p.p1 * z + h * h * (fk1 * p.ps - (fk1 - fk) * p.om);
+    int f = T.fframe[k];
+    if (f != fa.cur) {
+      if (fa.cur >= 0) flush(fa.cur);
+      fa.cur = f;
+      fa.A = 0.0;
+    }
+    fa.A += s;
+    z = p.e * z + h * (fk * p.ch + fk1 * p.ps);
+  }
+  if (fa.cur >= 0) flush(fa.cur);
+}
+
+__global__ void __launch_bounds__(128) bank_kernel(const BankParams p, const PriorDev prior) {
+  uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= p.N) return;
+  float th[ABC_MAX_P];
+  int m = draw_theta(prior, i, th);
+  int kind = prior.m[m].kind;
+  float* out = p.bank + i * p.T.LS;
+  const Tables& T = p.T;
+  if (kind <= ABC_2TCM_REV) {
+    double K1 = th[0], k2 = th[1], k3 = th[2], k4 = th[3], Vb = th[4];
+    double s = k2 + k3 + k4;
+    double r = sqrt((k2 - k4) * (k2 - k4) + k3 * (k3 + 2.0 * (k2 + k4)));
+    double a2 = 0.5 * (s + r);
+    double a1 = (s + r) > 0.0 ? 2.0 * k2 * k4 / (s + r) : 0.0;
+    double den = a2 - a1;
+    double c1 = K1 * (k3 + k4 - a1) / den;
+    double c2 = K1 * (a2 - k3 - k4) / den;
+    if (T.feng) sim_2tcm_feng(T, a1, a2, c1, c2, Vb, out);
+    else sim_2tcm_pwl(T, a1, a2, c1, c2, Vb, out);
+  } else if (kind == ABC_MRTM) {
+    sim_mrtm(T, th[0], th[1], th[2], out);
+  } else {
+    sim_lpntpet(T, th, out);
+  }
+  for (uint32_t f = T.L; f < T.LS; ++f) out[f] = 0.0f;
+}
+
+// ---- K1b: per-frame spread of the prescaled bank over a strided sample of draws ----
+__global__ void __launch_bounds__(256) frame_var_kernel(const OrderParams p) {
+  uint32_t f = blockIdx.x;
+  uint64_t stride = p.N > 65536 ? p.N / 65536 : 1;
+  uint64_t ns = (p.N + stride - 1) / stride;
+  double s1 = 0.0, s2 = 0.0;
+  double sc = p.wsc[f];
+  for (uint64_t j = threadIdx.x; j < ns; j += blockDim.x) {
+    double x = sc * double(p.bank[j * stride * p.LS + f]);
+    s1 += x;
+    s2 += x * x;
+  }
+  __shared__ double r1[256], r2[256];
+  r1[threadIdx.x] = s1;
+  r2[threadIdx.x] = s2;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      r1[threadIdx.x] += r1[threadIdx.x + o];
+      r2[threadIdx.x] += r2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double m = r1[0] / double(ns);
+    p.var[f] = fmax(r2[0] / double(ns) - m * m, 0.0);
+  }
+}
+
+// ---- K1b: descending-spread permutation (ties by frame index), padded with -1 ----
+__global__ void frame_perm_kernel(const OrderParams p) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int order[kMaxLP];
+  for (uint32_t f = 0; f < p.L; ++f) order[f] = int(f);
+  if (p.reorder) {
+    for (uint32_t a = 1; a < p.L; ++a) {  // insertion sort, stable
+      int x = order[a];
+      int b = int(a) - 1;
+      while (b >= 0 && p.var[order[b]] < p.var[x]) {
+        order[b + 1] = order[b];
+        --b;
+      }
+      order[b + 1] = x;
+    }
+  }
+  for (uint32_t k = 0; k < p.LP; ++k) {
+    int src = k < p.L ? order[k] : -1;
+    p.perm[k] = src;
+    p.wsp[k] = src >= 0 ? p.wsc[src] : 0.0f;
+  }
+}
+
+// ---- K1c: bankp[i][k] = -(wsp[k] * bank[i][perm[k]]) (scan order, negated, prescaled) ----
+__global__ void __launch_bounds__(256) permute_kernel(const OrderParams p) {
+  __shared__ int sperm[kMaxLP];
+  __shared__ float swsp[kMaxLP];
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    sperm[k] = p.perm[k];
+    swsp[k] = p.wsp[k];
+  }
+  __syncthreads();
+  uint64_t total = p.N * p.LP;
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t i = e / p.LP;
+    uint32_t k = uint32_t(e - i * p.LP);
+    int src = sperm[k];
+    float v = 0.0f;
+    if (src >= 0) v = -__fmul_rn(swsp[k], __ldg(p.bank + i * p.LS + src));
+    p.bankp[e] = v;
+  }
+}
+
+__global__ void fill_u32_kernel(uint32_t* p, uint32_t v, uint64_t n) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x)
+    p[e] = v;
+}
+
+}  // namespace
+
+void launch_bank(const BankParams& p, const PriorDev& prior, cudaStream_t st) {
+  uint64_t blocks = (p.N + 127) / 128;
+  bank_kernel<<<unsigned(blocks), 128, 0, st>>>(p, prior);
+}
+
+void launch_order(const OrderParams& p, cudaStream_t st) {
+  frame_var_kernel<<<p.L, 256, 0, st>>>(p);
+  frame_perm_kernel<<<1, 32, 0, st>>>(p);
+  permute_kernel<<<148 * 8, 256, 0, st>>>(p);
+}
+
+void launch_fill_u32(uint32_t* p, uint32_t v, uint64_t n, cudaStream_t st) {
+  fill_u32_kernel<<<148, 256, 0, st>>>(p, v, n);
+}
+
+}  // namespace vpet

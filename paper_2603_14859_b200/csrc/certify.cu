@@ -1,0 +1,404 @@
+// certify.cu -- K3 certification + K4 posterior reduction, the exact FP64 scan used as the
+// fallback (and as ABC_FLAG_EXACT), and the eps-mode reduction.
+//
+// K3 (warp per voxel): the FP32 pass left K = n + slack candidates (D32, i) per voxel.  Each is
+// re-scored in FP64 exactly as the oracle scores it (acquisition frame order, no contraction),
+// sorted by (D64, i) (ties -> lower index) and the first n kept.  The selection is
+// certified when every draw the FP32 pass excluded -- all have D32 >= tauK32, the largest kept
+// D32 -- provably has D > tau64 = the n-th D64:  tauK32 > tau64 + err(tau64) with err the
+// rigorous FP32 error bound.  Uncertified voxels go to the exact scan.
+// K4: per-model counts and probabilities, the preferred model (>50 %, P:282;
+// ties -> model 0), conditional mean, SD (ddof 1) and type-7 quantiles of every column over
+// the accepted draws of the preferred model, and K_i = K1 k3/(k2+k3).
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace vpet {
+namespace {
+
+__device__ __forceinline__ double exact_distance_c(const float* y, const float* s, const float* w, uint32_t L,
+                                                   int dist) {
+  double D = 0.0;
+  for (uint32_t f = 0; f < L; ++f) {
+    double d = __dsub_rn(double(__ldg(y + f)), double(__ldg(s + f)));
+    double t = (dist == ABC_DIST_L1) ? fabs(d) : __dmul_rn(d, d);
+    D = __dadd_rn(D, __dmul_rn(double(__ldg(w + f)), t));
+  }
+  return D;
+}
+
+__device__ __forceinline__ bool pair_gt(double a, uint32_t ia, double b, uint32_t ib) {
+  return a > b || (a == b && ia > ib);
+}
+
+// bitonic sort of (key, idx) pairs, ascending, n2 a power of two, one warp
+__device__ void warp_sort_pairs(double* key, uint32_t* idx, uint32_t n2, int lane) {
+  for (uint32_t size = 2; size <= n2; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t i = lane; i < n2; i += 32) {
+        uint32_t j = i ^ stride;
+        if (j > i) {
+          bool asc = (i & size) == 0;
+          double a = key[i], b = key[j];
+          uint32_t ia = idx[i], ib = idx[j];
+          bool swap = asc ? pair_gt(a, ia, b, ib) : pair_gt(b, ib, a, ia);
+          if (swap) {
+            key[i] = b; key[j] = a;
+            idx[i] = ib; idx[j] = ia;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__device__ void warp_sort_keys(double* key, uint32_t n2, int lane) {
+  for (uint32_t size = 2; size <= n2; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t i = lane; i < n2; i += 32) {
+        uint32_t j = i ^ stride;
+        if (j > i) {
+          bool asc = (i & size) == 0;
+          double a = key[i], b = key[j];
+          if (asc ? (a > b) : (a < b)) {
+            key[i] = b;
+            key[j] = a;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__device__ __forceinline__ double quantile7(const double* x, uint32_t c, double q) {
+  double h = double(c - 1) * q;
+  uint32_t lo = uint32_t(floor(h));
+  if (lo + 1 >= c) return x[c - 1];
+  return x[lo] + (h - double(lo)) * (x[lo + 1] - x[lo]);
+}
+
+__device__ __forceinline__ bool column_exists(int kind, uint32_t k) {
+  if (kind == ABC_MRTM) return k <= 3;
+  return k < ((kind >= ABC_MRTM) ? 7u : 5u);
+}
+
+// Reduce the sorted accepted list (ci[0..n)) of voxel v.  sc: np2 doubles of scratch.
+__device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* ci, const double* cd, double* sc,
+                            uint32_t np2, int lane) {
+  const uint32_t n = p.n;
+  const uint32_t M = p.prior.M;
+  const abc_result& o = p.out;
+  for (uint32_t a = lane; a < n; a += 32) {
+    if (o.acc_idx) o.acc_idx[v * n + a] = ci[a];
+    if (o.acc_dist) o.acc_dist[v * n + a] = cd[a];
+  }
+  uint32_t cnt[ABC_MAX_MODELS] = {0, 0, 0, 0};
+  for (uint32_t base = 0; base < n; base += 32) {
+    uint32_t a = base + lane;
+    int m = (a < n) ? model_index(p.prior, ci[a]) : -1;
+#pragma unroll
+    for (int k = 0; k < ABC_MAX_MODELS; ++k) cnt[k] += __popc(__ballot_sync(0xffffffffu, m == k));
+  }
+  int pref = 0;
+  for (uint32_t m = 1; m < M; ++m)
+    if (cnt[m] > cnt[pref]) pref = int(m);
+  if (lane == 0) {
+    for (uint32_t m = 0; m < M; ++m) {
+      if (o.count) o.count[v * M + m] = cnt[m];
+      if (o.prob) o.prob[v * M + m] = float(double(cnt[m]) / double(n));
+    }
+    if (o.preferred) o.preferred[v] = pref;
+  }
+  const int kind = p.prior.m[pref].kind;
+  const uint32_t c = cnt[pref];
+  const bool tcm = kind <= ABC_2TCM_REV;
+  const float NANF = __int_as_float(0x7fc00000);
+  for (uint32_t k = 0; k <= p.P; ++k) {  // column P = K_i
+    const bool is_ki = (k == p.P);
+    if (is_ki && !tcm) {
+      if (lane == 0) {
+        if (o.ki_mean) o.ki_mean[v] = NANF;
+        if (o.ki_sd) o.ki_sd[v] = NANF;
+        if (o.ki_q) for (int t = 0; t < 3; ++t) o.ki_q[v * 3 + t] = NANF;
+      }
+      continue;
+    }
+    bool exists = c > 0 && (is_ki || column_exists(kind, k));
+    float mean = NANF, sd = NANF, q3[3] = {NANF, NANF, NANF};
+    if (exists) {
+      uint32_t npos = 0;
+      double sum = 0.0;
+      for (uint32_t base = 0; base < n; base += 32) {
+        uint32_t a = base + lane;
+        bool mine = a < n && model_index(p.prior, ci[a]) == pref;
+        uint32_t bal = __ballot_sync(0xffffffffu, mine);
+        if (mine) {
+          float th[ABC_MAX_P];
+          draw_theta(p.prior, ci[a], th);
+          double x = is_ki ? double(th[0]) * double(th[2]) / (double(th[1]) + double(th[2])) : double(th[k]);
+          uint32_t pos = npos + __popc(bal & ((1u << lane) - 1u));
+          sc[pos] = x;
+          sum += x;
+        }
+        npos += __popc(bal);
+      }
+      sum = warp_sum(sum);
+      double mu = sum / double(c);
+      __syncwarp();
+      double ss = 0.0;
+      for (uint32_t a = lane; a < c; a += 32) ss += (sc[a] - mu) * (sc[a] - mu);
+      ss = warp_sum(ss);
+      for (uint32_t a = c + lane; a < np2; a += 32) sc[a] = __longlong_as_double(0x7ff0000000000000ll);
+      __syncwarp();
+      warp_sort_keys(sc, np2, lane);
+      mean = float(mu);
+      sd = c >= 2 ? float(sqrt(ss / double(c - 1))) : NANF;
+      q3[0] = float(quantile7(sc, c, 0.025));
+      q3[1] = float(quantile7(sc, c, 0.5));
+      q3[2] = float(quantile7(sc, c, 0.975));
+      __syncwarp();
+    }
+    if (lane == 0) {
+      if (is_ki) {
+        if (o.ki_mean) o.ki_mean[v] = mean;
+        if (o.ki_sd) o.ki_sd[v] = sd;
+        if (o.ki_q) for (int t = 0; t < 3; ++t) o.ki_q[v * 3 + t] = q3[t];
+      } else {
+        if (o.mean) o.mean[v * p.P + k] = mean;
+        if (o.sd) o.sd[v * p.P + k] = sd;
+        if (o.q) for (int t = 0; t < 3; ++t) o.q[(v * p.P + k) * 3 + t] = q3[t];
+      }
+    }
+  }
+}
+
+__global__ void certify_reduce_kernel(const ReduceParams p, uint32_t Kp, uint32_t np2, uint32_t wpc) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const uint32_t w = threadIdx.x >> 5;
+  const size_t per_warp = size_t(Kp) * 12 + size_t(np2) * 8;
+  double* cd = reinterpret_cast<double*>(smem_raw + per_warp * w);
+  double* sc = cd + Kp;
+  uint32_t* ci = reinterpret_cast<uint32_t*>(sc + np2);
+  const uint64_t len = p.list_len ? uint64_t(*p.list_len) : p.J;
+  const uint64_t nwarps = uint64_t(gridDim.x) * wpc;
+  const double DINF = __longlong_as_double(0x7ff0000000000000ll);
+  for (uint64_t e = uint64_t(blockIdx.x) * wpc + w; e < len; e += nwarps) {
+    const uint64_t v = p.list ? p.list[e] : e;
+    const float* y = p.tacs + v * p.L;
+    uint32_t cnt;
+    float tK = 0.0f;
+    if (p.exact) {
+      cnt = p.n;
+      for (uint32_t a = lane; a < Kp; a += 32) {
+        cd[a] = a < cnt ? p.hd[v * p.n + a] : DINF;
+        ci[a] = a < cnt ? p.hidx[v * p.n + a] : 0xffffffffu;
+      }
+    } else {
+      cnt = p.heap_cnt[v];
+      const uint32_t need = uint32_t(uint64_t(p.K) < p.N ? uint64_t(p.K) : p.N);
+      if (cnt < need) {  // heap never filled (non-finite FP32 distances): exact path
+        if (lane == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+        continue;
+      }
+      float tmax = 0.0f;
+      for (uint32_t a = lane; a < Kp; a += 32) {
+        if (a < cnt) {
+          unsigned long long key = p.heap[v * p.K + a];
+          uint32_t idx = uint32_t(key & 0xffffffffull);
+          tmax = fmaxf(tmax, __uint_as_float(uint32_t(key >> 32)));
+          cd[a] = exact_distance_c(y, p.bank + uint64_t(idx) * p.LS, p.w, p.L, p.dist);
+          ci[a] = idx;
+        } else {
+          cd[a] = DINF;
+          ci[a] = 0xffffffffu;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+      tK = tmax;
+    }
+    __syncwarp();
+    warp_sort_pairs(cd, ci, Kp, lane);
+    if (!p.exact && uint64_t(p.K) < p.N) {
+      double Y2 = 0.0, Y1 = 0.0;
+      for (uint32_t f = lane; f < p.L; f += 32) {
+        double yv = __ldg(y + f), wv = __ldg(p.w + f);
+        Y2 += wv * yv * yv;
+        Y1 += wv * fabs(yv);
+      }
+      Y2 = warp_sum(Y2);
+      Y1 = warp_sum(Y1);
+      double t64 = cd[p.n - 1];
+      double err = p.eb.a * t64 + p.eb.b * sqrt(Y2 * t64) + p.eb.c * Y2 + p.eb.d * Y1;
+      bool ok = double(tK) > t64 + err;
+      if (!ok) {
+        if (lane == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+        continue;
+      }
+    }
+    reduce_topn(p, v, ci, cd, sc, np2, lane);
+    __syncwarp();
+  }
+}
+
+// ---- exact FP64 scan: thread per voxel, max-heap of (D64, i) of size n, prefix pruning ----
+__device__ __noinline__ double exact_push(double* hd, uint32_t* hi, uint32_t n, uint32_t& cnt, double D, uint32_t idx) {
+  if (cnt < n) {
+    uint32_t pos = cnt++;
+    while (pos > 0) {
+      uint32_t par = (pos - 1) >> 1;
+      if (pair_gt(D, idx, hd[par], hi[par])) {  // new key above its parent: move parent down
+        hd[pos] = hd[par];
+        hi[pos] = hi[par];
+        pos = par;
+      } else {
+        break;
+      }
+    }
+    hd[pos] = D;
+    hi[pos] = idx;
+  } else {
+    uint32_t pos = 0;
+    for (;;) {
+      uint32_t l = 2 * pos + 1;
+      if (l >= n) break;
+      uint32_t c = l;
+      if (l + 1 < n && pair_gt(hd[l + 1], hi[l + 1], hd[l], hi[l])) c = l + 1;
+      if (!pair_gt(hd[c], hi[c], D, idx)) break;
+      hd[pos] = hd[c];
+      hi[pos] = hi[c];
+      pos = c;
+    }
+    hd[pos] = D;
+    hi[pos] = idx;
+  }
+  return cnt >= n ? hd[0] : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+__global__ void __launch_bounds__(64) exact_scan_kernel(const ExactParams p) {
+  const uint64_t len = p.list_len ? uint64_t(*p.list_len) : p.J;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < len; e += stride) {
+    const uint64_t v = p.list ? p.list[e] : e;
+    const float* y = p.tacs + v * p.L;
+    double* hd = p.hd + v * p.n;
+    uint32_t* hi = p.hi + v * p.n;
+    uint32_t cnt = 0;
+    double tau = __longlong_as_double(0x7ff0000000000000ll);
+    for (uint64_t i = 0; i < p.N; ++i) {
+      const float* s = p.bank + i * p.LS;
+      double D = 0.0;
+      bool rej = false;
+      for (uint32_t f = 0; f < p.L; ++f) {
+        double d = __dsub_rn(double(__ldg(y + f)), double(__ldg(s + f)));
+        double t = (p.dist == ABC_DIST_L1) ? fabs(d) : __dmul_rn(d, d);
+        D = __dadd_rn(D, __dmul_rn(double(__ldg(p.w + f)), t));
+        if (D >= tau) { rej = true; break; }  // prefix sums are monotone: D_final >= tau
+      }
+      if (!rej && D < tau) tau = exact_push(hd, hi, p.n, cnt, D, uint32_t(i));
+    }
+  }
+}
+
+// ---- eps mode: moments -> summaries (thread per voxel) ----
+__global__ void eps_reduce_kernel(const EpsReduceParams p) {
+  uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= p.J) return;
+  const uint32_t M = p.prior.M;
+  const double* mom = p.mom + v * size_t(M) * MOMW;
+  const abc_result& o = p.out;
+  const float NANF = __int_as_float(0x7fc00000);
+  double tot = 0.0;
+  int pref = -1;
+  double best = -1.0;
+  for (uint32_t m = 0; m < M; ++m) {
+    double c = mom[m * MOMW];
+    tot += c;
+    if (c > best) { best = c; pref = int(m); }
+  }
+  if (tot == 0.0) pref = -1;
+  for (uint32_t m = 0; m < M; ++m) {
+    double c = mom[m * MOMW];
+    if (o.count) o.count[v * M + m] = uint32_t(c);
+    if (o.prob) o.prob[v * M + m] = tot > 0.0 ? float(c / tot) : NANF;
+  }
+  if (o.preferred) o.preferred[v] = pref;
+  int kind = pref >= 0 ? p.prior.m[pref].kind : p.prior.m[0].kind;
+  double c = pref >= 0 ? mom[pref * MOMW] : 0.0;
+  const double* s = pref >= 0 ? mom + pref * MOMW : mom;
+  for (uint32_t k = 0; k < p.P; ++k) {
+    float mean = NANF, sd = NANF;
+    if (c > 0.0 && column_exists(kind, k)) {
+      double lo = p.prior.m[pref].lo[k];
+      double s1 = s[1 + 2 * k], s2 = s[2 + 2 * k];
+      mean = float(lo + s1 / c);
+      if (c >= 2.0) sd = float(sqrt(fmax(s2 - s1 * s1 / c, 0.0) / (c - 1.0)));
+    }
+    if (o.mean) o.mean[v * p.P + k] = mean;
+    if (o.sd) o.sd[v * p.P + k] = sd;
+    if (o.q) for (int t = 0; t < 3; ++t) o.q[(v * p.P + k) * 3 + t] = NANF;
+  }
+  float km = NANF, ks = NANF;
+  if (c > 0.0 && kind <= ABC_2TCM_REV) {
+    double s1 = s[1 + 2 * ABC_MAX_P], s2 = s[2 + 2 * ABC_MAX_P];
+    km = float(s1 / c);
+    if (c >= 2.0) ks = float(sqrt(fmax(s2 - s1 * s1 / c, 0.0) / (c - 1.0)));
+  }
+  if (o.ki_mean) o.ki_mean[v] = km;
+  if (o.ki_sd) o.ki_sd[v] = ks;
+  if (o.ki_q) for (int t = 0; t < 3; ++t) o.ki_q[v * 3 + t] = NANF;
+}
+
+uint32_t next_pow2(uint32_t x) {
+  uint32_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+void launch_certify_reduce(const ReduceParams& p, cudaStream_t st) {
+  uint32_t Kp = next_pow2(p.exact ? p.n : (p.K > p.n ? p.K : p.n));
+  if (Kp < 32) Kp = 32;
+  uint32_t np2 = next_pow2(p.n);
+  if (np2 < 32) np2 = 32;
+  size_t per_warp = size_t(Kp) * 12 + size_t(np2) * 8;
+  uint32_t wpc = 8;
+  while (wpc > 1 && per_warp * wpc > 96 * 1024) wpc >>= 1;
+  size_t smem = per_warp * wpc;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(certify_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = smem;
+  }
+  uint64_t work = p.list ? p.J : p.J;  // upper bound on list length
+  uint64_t blocks = (work + wpc - 1) / wpc;
+  if (blocks > 148ull * 64) blocks = 148ull * 64;
+  if (blocks == 0) blocks = 1;
+  certify_reduce_kernel<<<unsigned(blocks), wpc * 32, smem, st>>>(p, Kp, np2, wpc);
+}
+
+void launch_exact_scan(const ExactParams& p, cudaStream_t st) {
+  uint64_t blocks = (p.J + 63) / 64;
+  if (blocks > 148ull * 8) blocks = 148ull * 8;
+  if (blocks == 0) blocks = 1;
+  exact_scan_kernel<<<unsigned(blocks), 64, 0, st>>>(p);
+}
+
+void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st) {
+  uint64_t blocks = (p.J + 127) / 128;
+  if (blocks == 0) return;
+  eps_reduce_kernel<<<unsigned(blocks), 128, 0, st>>>(p);
+}
+
+}  // namespace vpet

@@ -1,0 +1,266 @@
+// common.cuh -- device-side building blocks shared by the kernels of libvpetabc.so.
+// (Independent of oracle/: nothing here is shared with the CPU oracle.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/vpetabc.h"
+
+namespace vpet {
+
+constexpr uint32_t kCtrTag = 0x56504554u;  // "VPET": 4th Philox counter word (R7)
+constexpr int kMaxLP = 128;
+constexpr int kMaxGrid = 8192;  // max points of a draw-independent time grid
+
+// ---------------------------------------------------------------------------------------
+// Prior draw (Alg.1 l.1-2): Philox4x32-10 keyed by the seed, counter
+// {i_lo, i_hi, block, 'VPET'}; u = (2*(x>>9)+1) 2^-24; theta = fmaf(hi-lo, u, lo).
+// ---------------------------------------------------------------------------------------
+__host__ __device__ inline void philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                         uint32_t k1, uint32_t out[4]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#ifdef __CUDA_ARCH__
+    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+#else
+    uint64_t p0 = 0xD2511F53ull * c0, p1 = 0xCD9E8D57ull * c2;
+    uint32_t hi0 = uint32_t(p0 >> 32), lo0 = uint32_t(p0), hi1 = uint32_t(p1 >> 32), lo1 = uint32_t(p1);
+#endif
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+__host__ __device__ inline float u01(uint32_t x) {
+  return float(((x >> 9) << 1) | 1u) * 5.9604644775390625e-8f;  // * 2^-24 (exact)
+}
+
+// Model / prior description in device-friendly form (constant memory).
+struct ModelDev {
+  int32_t kind;
+  uint32_t P;          // columns of the family (5 or 7)
+  uint64_t begin, end; // draw-index block [begin, end)
+  float lo[ABC_MAX_P], span[ABC_MAX_P];  // span = fl32(hi - lo)
+};
+struct PriorDev {
+  uint32_t M;
+  uint32_t seed_lo, seed_hi;
+  ModelDev m[ABC_MAX_MODELS];
+};
+
+__host__ __device__ inline int model_index(const PriorDev& pr, uint64_t i) {
+  int m = 0;
+#pragma unroll
+  for (int k = 1; k < ABC_MAX_MODELS; ++k)
+    if (k < (int)pr.M && i >= pr.m[k].begin) m = k;
+  return m;
+}
+
+// theta columns of draw i (P columns; IRR k4 := 0, MRTM gamma := 0, RT column 5 = tD + offset)
+__host__ __device__ inline int draw_theta(const PriorDev& pr, uint64_t i, float th[ABC_MAX_P]) {
+  int m = model_index(pr, i);
+  const ModelDev& md = pr.m[m];
+  uint32_t w[8];
+  philox10(uint32_t(i), uint32_t(i >> 32), 0u, kCtrTag, pr.seed_lo, pr.seed_hi, w);
+  philox10(uint32_t(i), uint32_t(i >> 32), 1u, kCtrTag, pr.seed_lo, pr.seed_hi, w + 4);
+#pragma unroll
+  for (int k = 0; k < ABC_MAX_P; ++k) th[k] = (k < (int)md.P) ? fmaf(md.span[k], u01(w[k]), md.lo[k]) : 0.0f;
+  if (md.kind == ABC_2TCM_IRR || md.kind == ABC_MRTM) th[3] = 0.0f;
+#ifdef __CUDA_ARCH__
+  if (md.kind >= ABC_MRTM) th[5] = __fadd_rn(th[4], th[5]);
+#else
+  if (md.kind >= ABC_MRTM) th[5] = th[4] + th[5];
+#endif
+  return m;
+}
+
+// ---------------------------------------------------------------------------------------
+// Exponential-integral phi functions (exact integration of a linear input against e^{-a t}
+// over a step of length h, x = a h):
+//   p1 = (1-e^-x)/x, ps = (x-1+e^-x)/x^2, ch = p1 - ps = (1-e^-x(1+x))/x^2,
+//   om = (x^2/2-1+e^-x(1+x))/x^3;  e = e^-x.
+// Series (Horner, 18 terms) below x = 0.5, closed forms above.
+// ---------------------------------------------------------------------------------------
+struct Phi {
+  double e, p1, ps, ch, om;
+};
+
+__device__ inline Phi phi_all(double x) {
+  Phi r;
+  if (x < 0.5) {
+    // coefficients: p1: 1/(k+1)!, ps: 1/(k+2)!, ch: (k+1)/(k+2)!, om: (k+2)/(k+3)!, alternating.
+    double p1 = 0.0, ps = 0.0, ch = 0.0, om = 0.0;
+    double f1 = 1.0 / 6402373705728000.0;  // 1/18!
+    double f2 = f1 / 19.0, f3 = f2 / 20.0;  // 1/19!, 1/20!
+#pragma unroll
+    for (int k = 17; k >= 0; --k) {
+      // f1 = 1/(k+1)!, f2 = 1/(k+2)!, f3 = 1/(k+3)!
+      p1 = fma(p1, -x, f1);
+      ps = fma(ps, -x, f2);
+      ch = fma(ch, -x, double(k + 1) * f2);
+      om = fma(om, -x, double(k + 2) * f3);
+      f3 = f2; f2 = f1; f1 = f1 * double(k + 1);
+    }
+    r.p1 = p1; r.ps = ps; r.ch = ch; r.om = om;
+    r.e = exp(-x);
+  } else {
+    double e = exp(-x), em1 = -expm1(-x);  // 1 - e^-x
+    double ix = 1.0 / x;
+    r.e = e;
+    r.p1 = em1 * ix;
+    r.ps = (x - em1) * ix * ix;
+    r.ch = (em1 - x * e) * ix * ix;
+    r.om = (0.5 * x * x - em1 + x * e) * ix * ix * ix;
+  }
+  return r;
+}
+
+// (1 - e^-x)/x for x >= 0; expm1 keeps full relative accuracy as x -> 0.
+__device__ inline double phi1_only(double x) { return x == 0.0 ? 1.0 : -expm1(-x) / x; }
+
+// ---------------------------------------------------------------------------------------
+// Launch-side helpers
+// ---------------------------------------------------------------------------------------
+struct Tables {
+  // frames (acquisition order)
+  uint32_t L, LS;          // frames, padded stride of the exact bank
+  const double* fdur;      // [L]
+  const double* fs;        // [L] starts
+  const double* fe;        // [L] ends
+  const double* favg_in;   // [L] int_frame C_in dt (draw independent)
+  const float* w;          // [L] weights (1 if none)
+  // coarse grid (PWL input U frame bounds)
+  uint32_t G;
+  const double* gt;        // [G]
+  const double* gc;        // [G] input value at grid points
+  const int* gframe;       // [G-1] frame of segment k or -1
+  // fine grid (lp-ntPET)
+  uint32_t GF;
+  const double* ft;
+  const double* fc;
+  const int* fframe;
+  // Feng input
+  int feng;
+  double fb[6];
+};
+
+struct BankParams {
+  Tables T;
+  uint64_t N;
+  float* bank;  // [N][LS] RN32 frame averages, acquisition order, zero padded
+};
+
+void launch_bank(const BankParams& p, const PriorDev& prior, cudaStream_t st);
+
+struct OrderParams {
+  const float* bank;  // [N][LS]
+  uint64_t N;
+  uint32_t L, LS, LP;
+  const float* wsc;   // [L] prescale factor per frame (sqrt(w) for WL2, w for L1, 1 if unit)
+  double* var;        // [L] scratch
+  int* perm;          // [LP] out: source frame of scan position k (-1 = pad)
+  float* wsp;         // [LP] out: prescale factor of scan position k (0 for pad)
+  float* bankp;       // [N][LP] out: -(wsp[k] * bank[i][perm[k]])
+  int reorder;
+};
+void launch_order(const OrderParams& p, cudaStream_t st);
+
+// Rigorous bound on |D32 - D| for the FP32 pass:
+//   err(D) = a D + b sqrt(Y2 D) + c Y2 + d Y1,  Y2 = sum_f w_f y_f^2, Y1 = sum_f w_f |y_f|.
+struct ErrBound {
+  double a, b, c, d;
+};
+
+struct ScanParams {
+  const float* bankp;   // [N][LP] negated prescaled bank in scan order
+  uint64_t N;
+  const float* tacs;    // [J][L]
+  uint64_t J;
+  uint32_t L;
+  const int* perm;      // [LP]
+  const float* wsp;     // [LP]
+  uint32_t K;           // heap capacity per voxel (top-n mode)
+  unsigned long long* heap;  // [J][K] keys (D32 bits << 32 | idx)
+  uint32_t* heap_cnt;   // [J]
+  int prune;
+  unsigned long long* work;  // frame-update counter (COUNT)
+  // eps mode
+  int eps_mode;
+  double eps;
+  const float* w;       // [L] weights (acquisition order), for inline FP64 rescoring
+  const float* bank;    // [N][LS] exact bank
+  uint32_t LS;
+  int dist;             // ABC_DIST_*
+  int unit_w;
+  double* mom;          // [J][M][MOMW] eps-mode moment sums
+  ErrBound eb;
+  const PriorDev* prior_g;  // device copy of the prior (eps-mode slow path)
+  uint32_t M;
+};
+constexpr int MOMW = 2 + 2 * ABC_MAX_P + 2;  // count, (S1,S2) x P, (KS1, KS2), pad
+cudaError_t launch_scan(const ScanParams& p, uint32_t LP, int count_work, cudaStream_t st);
+bool scan_supported(uint32_t LP);
+uint32_t scan_lp_for(uint32_t L);
+
+struct ExactParams {
+  const float* bank;  // [N][LS]
+  uint64_t N;
+  uint32_t L, LS;
+  const float* tacs;  // [J][L]
+  const float* w;     // [L]
+  int dist;
+  uint32_t n;
+  const uint32_t* list;  // voxel list (nullptr = all voxels 0..J-1)
+  const uint32_t* list_len;  // device count (nullptr = J)
+  uint64_t J;
+  double* hd;         // [J][n] exact heap distances
+  uint32_t* hi;       // [J][n] exact heap indices
+};
+void launch_exact_scan(const ExactParams& p, cudaStream_t st);
+
+struct ReduceParams {
+  // candidates
+  int exact;                    // 1: candidates from the exact heap (no certification)
+  const unsigned long long* heap;  // fast mode
+  const uint32_t* heap_cnt;
+  uint32_t K;
+  const double* hd;             // exact mode
+  const uint32_t* hidx;
+  const uint32_t* list;         // voxel list or nullptr
+  const uint32_t* list_len;
+  uint64_t J;
+  uint32_t n;
+  // data
+  const float* bank;  // [N][LS]
+  uint64_t N;
+  uint32_t L, LS, LP;
+  const float* tacs;
+  const float* w;
+  int dist;
+  int unit_w;
+  ErrBound eb;
+  PriorDev prior;
+  uint32_t P;
+  // fallback output
+  uint32_t* fb_list;
+  uint32_t* fb_len;
+  // results (device pointers, may be null)
+  abc_result out;
+};
+void launch_certify_reduce(const ReduceParams& p, cudaStream_t st);
+
+struct EpsReduceParams {
+  const double* mom;
+  uint64_t J;
+  PriorDev prior;
+  uint32_t P;
+  abc_result out;
+};
+void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st);
+
+void launch_fill_u32(uint32_t* p, uint32_t v, uint64_t n, cudaStream_t st);
+
+}  // namespace vpet

@@ -1,0 +1,159 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element, on
+seeded synthetic inputs shaped like the paper's workloads (BASELINE.json configs)."""
+import numpy as np
+import pytest
+
+import synthetic as S
+from tests.parity import compare, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    return S.config1()
+
+
+@pytest.fixture(scope="module")
+def tb_small():
+    # config-4-shaped: TB phantom voxels, PWL IDIF, 35 frames, IRR vs REV, n = 18
+    return S.config4_chunk(chunk=7, n_chunks=64, N=40_000, n=18, max_voxels=700)
+
+
+@pytest.fixture(scope="module")
+def rt_small():
+    # config-2-shaped: lp-ntPET vs MRTM, 61 frames, PWL reference TAC
+    return S.config2(J=96, N_per_model=4000, n=40, noise="mid")
+
+
+def test_bank_matches_oracle_rn32(cfg1, tb_small, rt_small):
+    """Alg.1 l.3: the GPU bank equals the oracle's RN32 frame averages (rare 1-ulp flips of
+    values within FP64 rounding of an FP32 tie are allowed)."""
+    for prob in (cfg1, tb_small, rt_small):
+        small = prob.replace(models=[dict(m, n_draws=min(int(m["n_draws"]), 3000)) for m in prob.ctx_kwargs["models"]],
+                             n_accept=5)
+        _, g = run_gpu(small, tacs=small.tacs[:4])
+        _, o = run_oracle(small, tacs=small.tacs[:4])
+        gb, ob = g.bank(), o.bank()
+        diff = gb != ob
+        assert diff.mean() < 1e-4, (prob.name, int(diff.sum()))
+        np.testing.assert_allclose(gb, ob, rtol=2.5e-7, atol=0)
+
+
+def test_config1_topn_wl2(cfg1):
+    g, gc = run_gpu(cfg1, flags=1)
+    o, _ = run_oracle(cfg1)
+    rep = compare(g, o)
+    assert rep["matched"] >= cfg1.J - 1
+    st = gc.stats()
+    assert st["gpu_launches"] >= 5 and st["n_voxels"] == cfg1.J
+
+
+@pytest.mark.parametrize("distance", ["L1", "WL2"])
+@pytest.mark.parametrize("weighted", [True, False])
+def test_config1_distances_and_weights(cfg1, distance, weighted):
+    p = cfg1.replace(distance=distance)
+    if not weighted:
+        import dataclasses
+        p = dataclasses.replace(p, weight=None)
+    g, _ = run_gpu(p)
+    o, _ = run_oracle(p)
+    compare(g, o)
+
+
+def test_tb_model_selection(tb_small):
+    g, gc = run_gpu(tb_small)
+    o, _ = run_oracle(tb_small)
+    rep = compare(g, o)
+    assert rep["matched"] >= tb_small.J - 2
+
+
+def test_rt_model_selection(rt_small):
+    g, _ = run_gpu(rt_small)
+    o, _ = run_oracle(rt_small)
+    compare(g, o)
+
+
+@pytest.mark.parametrize("flags", [0x2, 0x8, 0x10, 0x8 | 0x10])
+def test_exact_noprune_noreorder_identical(tb_small, flags):
+    """ABC_FLAG_EXACT (pure FP64 scan), NO_PRUNE and NO_REORDER give the same accepted sets."""
+    sub = tb_small.subset(np.arange(130))
+    base, _ = run_gpu(sub)
+    alt, _ = run_gpu(sub, flags=flags)
+    for k in base:
+        np.testing.assert_array_equal(np.nan_to_num(base[k]), np.nan_to_num(alt[k]), err_msg=k)
+
+
+def test_eps_mode(cfg1):
+    """eps mode: accept D <= eps; moments from streaming sums."""
+    o_top, _ = run_oracle(cfg1)
+    eps = float(np.median(o_top["acc_dist"][:, -1]))
+    p = cfg1.replace(accept="EPS", epsilon=eps)
+    g, _ = run_gpu(p)
+    o, _ = run_oracle(p)
+    assert np.array_equal(g["count"], o["count"])
+    compare(g, o, topn=False)
+    # eps -> inf accepts every draw: prior moments
+    p2 = cfg1.replace(accept="EPS", epsilon=1e300)
+    g2, _ = run_gpu(p2, tacs=cfg1.tacs[:3])
+    o2, _ = run_oracle(p2, tacs=cfg1.tacs[:3])
+    assert np.all(g2["count"] == 10_000)
+    compare(g2, o2, topn=False)
+
+
+@pytest.mark.parametrize("J", [1, 31, 513, 1025])
+def test_ragged_voxel_counts(tb_small, J):
+    idx = np.arange(J) % tb_small.J
+    sub = tb_small.subset(idx)
+    g, _ = run_gpu(sub)
+    o, _ = run_oracle(sub)
+    compare(g, o)
+
+
+@pytest.mark.parametrize("N,n", [(7, 3), (64, 64), (65, 1), (1000, 1000 // 8)])
+def test_small_and_degenerate_budgets(cfg1, N, n):
+    """N < tile, N = one tile, n = N (everything accepted), n = 1."""
+    p = cfg1.replace(models=[dict(cfg1.ctx_kwargs["models"][0], n_draws=N)], n_accept=n)
+    sub = p.subset(np.arange(40))
+    g, _ = run_gpu(sub)
+    o, _ = run_oracle(sub)
+    compare(g, o)
+
+
+def test_zero_voxels_and_errors(cfg1):
+    from paper_2603_14859_b200 import AbcContext, AbcError
+    ctx = AbcContext(**cfg1.ctx_kwargs)
+    with pytest.raises(AbcError) as e:
+        ctx.run_voxels(cfg1.tacs)
+    assert e.value.status == 2  # state: nothing set
+    cfg1.setup(ctx)
+    r = ctx.run_voxels(np.zeros((0, cfg1.L), np.float32))
+    assert r["prob"].shape == (0, 1)
+    bad = cfg1.tacs[:4].copy()
+    bad[2, 5] = np.nan
+    with pytest.raises(AbcError) as e:
+        ctx.run_voxels(bad)
+    assert e.value.status == 1
+
+
+def test_device_pointers_and_stream(tb_small):
+    import torch
+    from paper_2603_14859_b200 import AbcContext
+    ctx = AbcContext(**tb_small.ctx_kwargs)
+    tb_small.setup(ctx)
+    s = torch.cuda.Stream()
+    ctx.set_stream(s.cuda_stream)
+    y = torch.from_numpy(tb_small.tacs).cuda()
+    with torch.cuda.stream(s):
+        rd = ctx.run_voxels(y)
+    torch.cuda.synchronize()
+    ctx.set_stream(None)
+    rh = ctx.run_voxels(tb_small.tacs)
+    for k in rh:
+        a = rd[k].cpu().numpy()
+        b = rh[k]
+        if b.dtype == np.uint64:
+            a = a.astype(np.uint64)
+        if b.dtype == np.uint32:
+            a = a.astype(np.uint32)
+        np.testing.assert_array_equal(np.nan_to_num(a), np.nan_to_num(b), err_msg=k)
