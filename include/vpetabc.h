@@ -88,6 +88,7 @@ typedef enum { ABC_INPUT_PWL = 0, ABC_INPUT_FENG = 1 } abc_input_kind;
 #define ABC_FLAG_COUNT_WORK 0x4u /* count executed frame updates of the FP32 pass */
 #define ABC_FLAG_NO_PRUNE 0x8u   /* FP32 pass evaluates all frames of every pair (A/B only) */
 #define ABC_FLAG_NO_REORDER 0x10u/* FP32 pass keeps the acquisition frame order (A/B only) */
+#define ABC_FLAG_NO_TREE 0x20u   /* FP32 pass scans every draw in index order, no bounds (A/B only) */
 
 /* abc_run_voxels ptr_flags */
 #define ABC_PTR_TACS_DEVICE 0x1u /* tacs is a device pointer on ctx's device */
@@ -142,7 +143,8 @@ typedef struct abc_stats {
   uint64_t n_voxels;
   uint64_t n_draws;
   uint64_t n_fallback;        /* voxels whose FP32 pass could not be certified (re-run exactly) */
-  uint64_t frame_updates;     /* executed FP32 frame updates (ABC_FLAG_COUNT_WORK) */
+  uint64_t frame_updates;     /* executed FP32 frame updates of draw evaluations (ABC_FLAG_COUNT_WORK) */
+  uint64_t bound_updates;     /* executed FP32 frame updates of (super-)tile lower bounds (idem) */
   uint32_t lp;                /* padded frame count of the FP32 pass */
   uint32_t heap_k;            /* candidates kept per voxel by the FP32 pass */
   double ms_h2d, ms_bank, ms_order, ms_scan, ms_certify, ms_fallback, ms_d2h, ms_total;

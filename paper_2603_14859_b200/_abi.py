@@ -21,7 +21,7 @@ KINDS = {"2TCM_IRR": 0, "2TCM_REV": 1, "MRTM": 2, "LPNTPET": 3}
 DISTANCES = {"L1": 1, "WL2": 2}
 ACCEPTS = {"TOPN": 0, "EPS": 1}
 INPUTS = {"PWL": 0, "FENG": 1}
-FLAG_TIMING, FLAG_EXACT, FLAG_COUNT_WORK, FLAG_NO_PRUNE, FLAG_NO_REORDER = 0x1, 0x2, 0x4, 0x8, 0x10
+FLAG_TIMING, FLAG_EXACT, FLAG_COUNT_WORK, FLAG_NO_PRUNE, FLAG_NO_REORDER, FLAG_NO_TREE = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 PTR_TACS_DEVICE, PTR_OUT_DEVICE = 0x1, 0x2
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_STATE", 3: "E_NOMEM", 4: "E_CUDA", 5: "E_UNSUPPORTED"}
 
@@ -52,6 +52,7 @@ class Result(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("gpu_launches", C.c_uint32), ("n_voxels", C.c_uint64),
                 ("n_draws", C.c_uint64), ("n_fallback", C.c_uint64), ("frame_updates", C.c_uint64),
+                ("bound_updates", C.c_uint64),
                 ("lp", C.c_uint32), ("heap_k", C.c_uint32),
                 ("ms_h2d", C.c_double), ("ms_bank", C.c_double), ("ms_order", C.c_double),
                 ("ms_scan", C.c_double), ("ms_certify", C.c_double), ("ms_fallback", C.c_double),

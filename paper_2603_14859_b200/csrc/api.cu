@@ -77,9 +77,11 @@ struct abc_ctx {
   uint32_t G = 0, GF = 0;
   DevBuf d_fdur, d_fs, d_fe, d_favg, d_w, d_wsc, d_gt, d_gc, d_gframe, d_ft, d_fc, d_fframe;
   // work buffers
-  DevBuf d_prior, bank, bankp, var, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
+  DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
+  DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds;
   abc_stats stats{};
   bool bank_valid = false;
+  bool dist_wl2() const { return cfg.distance == ABC_DIST_WL2; }
   uint32_t bank_L = 0;
   cudaEvent_t ev[EV_N] = {};
   bool ev_ok = false;
@@ -257,6 +259,25 @@ ErrBound error_bound(const abc_ctx* c, uint32_t LP) {
   }
   return e;
 }
+
+}  // namespace
+
+namespace vpet {
+// padded frame counts with a compiled FP32-pass instance (scan_kernels.cuh VPET_LP_LIST)
+static const uint32_t kLPs[] = {8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 56, 64, 80, 96, 128};
+bool scan_supported(uint32_t LP) {
+  for (uint32_t v : kLPs)
+    if (v == LP) return true;
+  return false;
+}
+uint32_t scan_lp_for(uint32_t L) {
+  for (uint32_t v : kLPs)
+    if (L <= v) return v;
+  return 0;
+}
+}  // namespace vpet
+
+namespace {
 
 __global__ void finite_check_kernel(const float* x, uint64_t n, int* flag) {
   for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x)
@@ -464,6 +485,10 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   size_t need = 0;
   need += sizeof(float) * N * LS;                        // exact bank
   if (!exact) need += sizeof(float) * N * LP;            // scan bank
+  const bool tree = !exact && !(ctx->cfg.flags & ABC_FLAG_NO_TREE) && N < (1ull << 31);
+  const uint64_t ntile = (N + kTile - 1) / kTile, nsuper = (ntile + kSuper - 1) / kSuper;
+  const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
+  if (tree) need += N * (8 + 8 + 4 + 4 + 4) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper);
   if (!eps) need += size_t(8) * J * K + 4 * J;           // heaps
   need += size_t(12) * J * (n ? n : 1);                  // exact heaps (fallback)
   if (eps) need += sizeof(double) * J * M * MOMW;
@@ -478,6 +503,20 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   CK(ctx->bank.ensure(sizeof(float) * N * LS));
   if (!exact) CK(ctx->bankp.ensure(sizeof(float) * N * LP));
   CK(ctx->var.ensure(sizeof(double) * kMaxLP));
+  CK(ctx->fmean.ensure(sizeof(double) * kMaxLP));
+  if (tree) {
+    CK(ctx->cov.ensure(sizeof(double) * kMaxLP * kMaxLP));
+    CK(ctx->pcs.ensure(sizeof(float) * kNPC * kMaxLP));
+    CK(ctx->pminmax.ensure(sizeof(unsigned int) * 2 * kNPC));
+    CK(ctx->keys.ensure(8 * N));
+    CK(ctx->keys_alt.ensure(8 * N));
+    CK(ctx->vals.ensure(4 * N));
+    CK(ctx->order.ensure(4 * N));
+    CK(ctx->idxmap.ensure(4 * (N + 4)));
+    CK(ctx->sort_temp.ensure(sort_tmp));
+    CK(ctx->tbounds.ensure(sizeof(float) * 2 * LP * ntile));
+    CK(ctx->sbounds.ensure(sizeof(float) * 2 * LP * nsuper));
+  }
   CK(ctx->perm.ensure(sizeof(int) * kMaxLP));
   CK(ctx->wsp.ensure(sizeof(float) * kMaxLP));
   if (!eps) {
@@ -555,12 +594,27 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     op.LP = LP;
     op.wsc = ctx->d_wsc.as<float>();
     op.var = ctx->var.as<double>();
+    op.mean = ctx->fmean.as<double>();
     op.perm = ctx->perm.as<int>();
     op.wsp = ctx->wsp.as<float>();
     op.bankp = ctx->bankp.as<float>();
     op.reorder = !(ctx->cfg.flags & ABC_FLAG_NO_REORDER);
-    launch_order(op, st);
-    launches += 3;
+    op.tree = tree;
+    if (tree) {
+      op.cov = ctx->cov.as<double>();
+      op.pcs = ctx->pcs.as<float>();
+      op.pminmax = ctx->pminmax.as<unsigned int>();
+      op.keys = ctx->keys.as<unsigned long long>();
+      op.keys_alt = ctx->keys_alt.as<unsigned long long>();
+      op.vals = ctx->vals.as<uint32_t>();
+      op.order = ctx->order.as<uint32_t>();
+      op.idxmap = ctx->idxmap.as<uint32_t>();
+      op.sort_temp = ctx->sort_temp.p;
+      op.sort_temp_bytes = sort_tmp;
+      op.tbounds = ctx->tbounds.as<float>();
+      op.sbounds = ctx->sbounds.as<float>();
+    }
+    CK(launch_order(op, st, &launches));
   }
   rec(EV_ORDER);
 
@@ -589,8 +643,16 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     sp.eb = eb;
     sp.prior_g = ctx->d_prior.as<PriorDev>();
     sp.M = M;
+    if (tree) {
+      sp.idxmap = ctx->idxmap.as<uint32_t>();
+      sp.tbounds = ctx->tbounds.as<float>();
+      sp.sbounds = ctx->sbounds.as<float>();
+      sp.ntile = ntile;
+      sp.nsuper = nsuper;
+    }
+    sp.bound_work = ctx->work.as<unsigned long long>() + 1;
     if (eps) CK(cudaMemsetAsync(ctx->mom.p, 0, sizeof(double) * J * M * MOMW, st));
-    CK(launch_scan(sp, LP, count_work, st));
+    CK(ctx->dist_wl2() ? launch_scan_wl2(sp, LP, count_work, tree, st) : launch_scan_l1(sp, LP, count_work, tree, st));
     ++launches;
   }
   rec(EV_SCAN);
@@ -677,14 +739,15 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   rec(EV_D2H);
   int h_flag = 0;
   uint32_t h_fb = 0;
-  unsigned long long h_work = 0;
+  unsigned long long h_work[2] = {0, 0};
   CK(cudaMemcpyAsync(&h_flag, ctx->flag.p, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&h_fb, ctx->fb_len.p, 4, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&h_work, ctx->work.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_work, ctx->work.p, 16, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   S.gpu_launches = launches;
   S.n_fallback = h_fb;
-  S.frame_updates = h_work;
+  S.frame_updates = h_work[0];
+  S.bound_updates = h_work[1];
   if (timing) {
     auto ms = [&](int a, int b) {
       float x = 0.0f;
@@ -731,6 +794,9 @@ void abc_destroy(abc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->dev);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  DevBuf* bufs2[] = {&ctx->fmean, &ctx->cov, &ctx->pcs, &ctx->pminmax, &ctx->keys, &ctx->keys_alt, &ctx->vals,
+                     &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds};
+  for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,
                     &ctx->bank,   &ctx->bankp, &ctx->var,    &ctx->perm,   &ctx->wsp,        &ctx->heap,

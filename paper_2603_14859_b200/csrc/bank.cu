@@ -1,5 +1,4 @@
-// bank.cu -- K1: simulation bank (Alg. 1 lines 1-3) and K1b/c: frame ordering and
-// the negated, prescaled scan-order copy used by the FP32 pass.
+// bank.cu -- K1: simulation bank (Alg. 1 lines 1-3).
 //
 // Each thread simulates one draw in FP64 and stores the frame averages rounded to FP32
 // (the method's FP32 TAC):
@@ -182,78 +181,6 @@ __global__ void __launch_bounds__(128) bank_kernel(const BankParams p, const Pri
   for (uint32_t f = T.L; f < T.LS; ++f) out[f] = 0.0f;
 }
 
-// ---- K1b: per-frame spread of the prescaled bank over a strided sample of draws ----
-__global__ void __launch_bounds__(256) frame_var_kernel(const OrderParams p) {
-  uint32_t f = blockIdx.x;
-  uint64_t stride = p.N > 65536 ? p.N / 65536 : 1;
-  uint64_t ns = (p.N + stride - 1) / stride;
-  double s1 = 0.0, s2 = 0.0;
-  double sc = p.wsc[f];
-  for (uint64_t j = threadIdx.x; j < ns; j += blockDim.x) {
-    double x = sc * double(p.bank[j * stride * p.LS + f]);
-    s1 += x;
-    s2 += x * x;
-  }
-  __shared__ double r1[256], r2[256];
-  r1[threadIdx.x] = s1;
-  r2[threadIdx.x] = s2;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      r1[threadIdx.x] += r1[threadIdx.x + o];
-      r2[threadIdx.x] += r2[threadIdx.x + o];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    double m = r1[0] / double(ns);
-    p.var[f] = fmax(r2[0] / double(ns) - m * m, 0.0);
-  }
-}
-
-// ---- K1b: descending-spread permutation (ties by frame index), padded with -1 ----
-__global__ void frame_perm_kernel(const OrderParams p) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int order[kMaxLP];
-  for (uint32_t f = 0; f < p.L; ++f) order[f] = int(f);
-  if (p.reorder) {
-    for (uint32_t a = 1; a < p.L; ++a) {  // insertion sort, stable
-      int x = order[a];
-      int b = int(a) - 1;
-      while (b >= 0 && p.var[order[b]] < p.var[x]) {
-        order[b + 1] = order[b];
-        --b;
-      }
-      order[b + 1] = x;
-    }
-  }
-  for (uint32_t k = 0; k < p.LP; ++k) {
-    int src = k < p.L ? order[k] : -1;
-    p.perm[k] = src;
-    p.wsp[k] = src >= 0 ? p.wsc[src] : 0.0f;
-  }
-}
-
-// ---- K1c: bankp[i][k] = -(wsp[k] * bank[i][perm[k]]) (scan order, negated, prescaled) ----
-__global__ void __launch_bounds__(256) permute_kernel(const OrderParams p) {
-  __shared__ int sperm[kMaxLP];
-  __shared__ float swsp[kMaxLP];
-  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
-    sperm[k] = p.perm[k];
-    swsp[k] = p.wsp[k];
-  }
-  __syncthreads();
-  uint64_t total = p.N * p.LP;
-  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
-    uint64_t i = e / p.LP;
-    uint32_t k = uint32_t(e - i * p.LP);
-    int src = sperm[k];
-    float v = 0.0f;
-    if (src >= 0) v = -__fmul_rn(swsp[k], __ldg(p.bank + i * p.LS + src));
-    p.bankp[e] = v;
-  }
-}
-
 __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, uint64_t n) {
   for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x)
     p[e] = v;
@@ -264,12 +191,6 @@ __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, uint64_t n) {
 void launch_bank(const BankParams& p, const PriorDev& prior, cudaStream_t st) {
   uint64_t blocks = (p.N + 127) / 128;
   bank_kernel<<<unsigned(blocks), 128, 0, st>>>(p, prior);
-}
-
-void launch_order(const OrderParams& p, cudaStream_t st) {
-  frame_var_kernel<<<p.L, 256, 0, st>>>(p);
-  frame_perm_kernel<<<1, 32, 0, st>>>(p);
-  permute_kernel<<<148 * 8, 256, 0, st>>>(p);
 }
 
 void launch_fill_u32(uint32_t* p, uint32_t v, uint64_t n, cudaStream_t st) {

@@ -10,6 +10,9 @@ namespace vpet {
 
 constexpr uint32_t kCtrTag = 0x56504554u;  // "VPET": 4th Philox counter word (R7)
 constexpr int kMaxLP = 128;
+constexpr int kNPC = 4;      // principal axes used for the draw order (order.cu)
+constexpr int kTile = 64;    // draws per tile (bounding box + TMA transfer unit)
+constexpr int kSuper = 16;   // tiles per super-tile
 constexpr int kMaxGrid = 8192;  // max points of a draw-independent time grid
 
 // ---------------------------------------------------------------------------------------
@@ -160,13 +163,29 @@ struct OrderParams {
   uint64_t N;
   uint32_t L, LS, LP;
   const float* wsc;   // [L] prescale factor per frame (sqrt(w) for WL2, w for L1, 1 if unit)
-  double* var;        // [L] scratch
+  double* var;        // [L] scratch: spread of the prescaled frame
+  double* mean;       // [L] scratch: mean of the prescaled frame
   int* perm;          // [LP] out: source frame of scan position k (-1 = pad)
   float* wsp;         // [LP] out: prescale factor of scan position k (0 for pad)
-  float* bankp;       // [N][LP] out: -(wsp[k] * bank[i][perm[k]])
+  float* bankp;       // [N][LP] out: -(wsp[k] * bank[order[j]][perm[k]])
   int reorder;
+  // locality order + bounds (tree mode)
+  int tree;
+  double* cov;        // [LP][LP]
+  float* pcs;         // [kNPC][LP]
+  unsigned int* pminmax;  // [kNPC][2] ordered-int min/max of the projections
+  unsigned long long* keys;      // [N]
+  unsigned long long* keys_alt;  // [N]
+  uint32_t* vals;     // [N]
+  uint32_t* order;    // [N] sorted position -> draw index
+  uint32_t* idxmap;   // [N] out: draw index of scan row j
+  void* sort_temp;
+  size_t sort_temp_bytes;
+  float* tbounds;     // [ntile][2][LP] per-tile min/max of bankp
+  float* sbounds;     // [nsuper][2][LP]
 };
-void launch_order(const OrderParams& p, cudaStream_t st);
+cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launches);
+size_t order_sort_temp_bytes(uint64_t N);
 
 // Rigorous bound on |D32 - D| for the FP32 pass:
 //   err(D) = a D + b sqrt(Y2 D) + c Y2 + d Y1,  Y2 = sum_f w_f y_f^2, Y1 = sum_f w_f |y_f|.
@@ -199,9 +218,17 @@ struct ScanParams {
   ErrBound eb;
   const PriorDev* prior_g;  // device copy of the prior (eps-mode slow path)
   uint32_t M;
+  // tree mode
+  const uint32_t* idxmap;   // [N] draw index of scan row j
+  const float* tbounds;     // [ntile][2][LP]
+  const float* sbounds;     // [nsuper][2][LP]
+  uint64_t ntile, nsuper;
+  unsigned long long* bound_work;  // LB frame-evaluation counter (COUNT)
 };
 constexpr int MOMW = 2 + 2 * ABC_MAX_P + 2;  // count, (S1,S2) x P, (KS1, KS2), pad
-cudaError_t launch_scan(const ScanParams& p, uint32_t LP, int count_work, cudaStream_t st);
+cudaError_t launch_scan(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);
+cudaError_t launch_scan_wl2(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);
+cudaError_t launch_scan_l1(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);
 bool scan_supported(uint32_t LP);
 uint32_t scan_lp_for(uint32_t L);
 

@@ -1,0 +1,343 @@
+// order.cu -- K1b/K1c: the scan-order copy of the bank and its bounding-box hierarchy.
+//
+// The FP32 pass visits frames in descending-spread order (frame_var/frame_perm) and draws in a
+// locality-preserving order: each draw's prescaled curve is projected on the top NPC principal
+// axes of the bank (covariance + power iteration), quantised on an isotropic grid and sorted by
+// its Morton code.  Consecutive draws are then close in TAC space, so the per-frame bounding
+// boxes of tiles of T draws (and of super-tiles of ST tiles) are tight and give exact lower
+// bounds on the FP32 discrepancy of every draw inside them (scan_tree.cu).  The order only
+// changes which draws are looked at first; selection is by (D, original index) keys.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace vpet {
+namespace {
+
+// ---- per-frame mean and spread of the prescaled bank over a strided sample ----
+__global__ void __launch_bounds__(256) frame_stats_kernel(const OrderParams p) {
+  uint32_t f = blockIdx.x;
+  uint64_t stride = p.N > 65536 ? p.N / 65536 : 1;
+  uint64_t ns = (p.N + stride - 1) / stride;
+  double s1 = 0.0, s2 = 0.0;
+  double sc = p.wsc[f];
+  for (uint64_t j = threadIdx.x; j < ns; j += blockDim.x) {
+    double x = sc * double(p.bank[j * stride * p.LS + f]);
+    s1 += x;
+    s2 += x * x;
+  }
+  __shared__ double r1[256], r2[256];
+  r1[threadIdx.x] = s1;
+  r2[threadIdx.x] = s2;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      r1[threadIdx.x] += r1[threadIdx.x + o];
+      r2[threadIdx.x] += r2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double m = r1[0] / double(ns);
+    p.var[f] = fmax(r2[0] / double(ns) - m * m, 0.0);
+    p.mean[f] = m;
+  }
+}
+
+// ---- descending-spread permutation (stable), padded with -1 ----
+__global__ void frame_perm_kernel(const OrderParams p) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int order[kMaxLP];
+  for (uint32_t f = 0; f < p.L; ++f) order[f] = int(f);
+  if (p.reorder) {
+    for (uint32_t a = 1; a < p.L; ++a) {
+      int x = order[a];
+      int b = int(a) - 1;
+      while (b >= 0 && p.var[order[b]] < p.var[x]) {
+        order[b + 1] = order[b];
+        --b;
+      }
+      order[b + 1] = x;
+    }
+  }
+  for (uint32_t k = 0; k < p.LP; ++k) {
+    int src = k < p.L ? order[k] : -1;
+    p.perm[k] = src;
+    p.wsp[k] = src >= 0 ? p.wsc[src] : 0.0f;
+  }
+}
+
+// ---- covariance of the prescaled bank (scan order), one block per (row, col) pair ----
+__global__ void __launch_bounds__(256) cov_kernel(const OrderParams p) {
+  uint32_t a = blockIdx.x, b = blockIdx.y;
+  if (b < a) return;
+  int fa = p.perm[a], fb = p.perm[b];
+  uint64_t stride = p.N > 16384 ? p.N / 16384 : 1;
+  uint64_t ns = (p.N + stride - 1) / stride;
+  double s = 0.0;
+  if (fa >= 0 && fb >= 0) {
+    double ma = p.mean[fa], mb = p.mean[fb], ca = p.wsc[fa], cb = p.wsc[fb];
+    for (uint64_t j = threadIdx.x; j < ns; j += blockDim.x) {
+      const float* row = p.bank + j * stride * p.LS;
+      s += (ca * double(row[fa]) - ma) * (cb * double(row[fb]) - mb);
+    }
+  }
+  __shared__ double r[256];
+  r[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) r[threadIdx.x] += r[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double c = r[0] / double(ns);
+    p.cov[a * p.LP + b] = c;
+    p.cov[b * p.LP + a] = c;
+  }
+}
+
+// ---- top-NPC eigenvectors by power iteration with deflation (one block) ----
+__global__ void __launch_bounds__(128) pca_kernel(const OrderParams p) {
+  __shared__ double C[kMaxLP * kMaxLP / 4];  // LP <= 128 handled in chunks below
+  __shared__ double v[kMaxLP], w[kMaxLP];
+  __shared__ double nrm;
+  const uint32_t LP = p.LP;
+  // C may not fit for LP = 128 (128 KB); work from global memory in that case.
+  const bool in_smem = LP * LP <= kMaxLP * kMaxLP / 4;
+  double* Cm = in_smem ? C : p.cov;
+  if (in_smem)
+    for (uint32_t e = threadIdx.x; e < LP * LP; e += blockDim.x) C[e] = p.cov[e];
+  __syncthreads();
+  for (int c = 0; c < kNPC; ++c) {
+    for (uint32_t k = threadIdx.x; k < LP; k += blockDim.x) v[k] = 1.0 + 0.001 * double((k * 7919u + c * 104729u) % 97u);
+    __syncthreads();
+    for (int it = 0; it < 400; ++it) {
+      for (uint32_t k = threadIdx.x; k < LP; k += blockDim.x) {
+        double s = 0.0;
+        for (uint32_t g = 0; g < LP; ++g) s += Cm[k * LP + g] * v[g];
+        w[k] = s;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (uint32_t k = 0; k < LP; ++k) s += w[k] * w[k];
+        nrm = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+      }
+      __syncthreads();
+      for (uint32_t k = threadIdx.x; k < LP; k += blockDim.x) v[k] = w[k] * nrm;
+      __syncthreads();
+    }
+    // eigenvalue and deflation
+    if (threadIdx.x == 0) {
+      double lam = 0.0;
+      for (uint32_t k = 0; k < LP; ++k) {
+        double s = 0.0;
+        for (uint32_t g = 0; g < LP; ++g) s += Cm[k * LP + g] * v[g];
+        lam += v[k] * s;
+      }
+      nrm = lam;
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < LP * LP; e += blockDim.x) Cm[e] -= nrm * v[e / LP] * v[e % LP];
+    for (uint32_t k = threadIdx.x; k < LP; k += blockDim.x) p.pcs[c * LP + k] = float(v[k]);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ unsigned int f2ord(float x) {
+  unsigned int u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned int u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__device__ __forceinline__ void project(const OrderParams& p, uint64_t i, const float* sm_mu, const float* sm_pc,
+                                        const int* sm_perm, const float* sm_wsp, float pr[kNPC]) {
+  const float* row = p.bank + i * p.LS;
+#pragma unroll
+  for (int c = 0; c < kNPC; ++c) pr[c] = 0.0f;
+  for (uint32_t k = 0; k < p.LP; ++k) {
+    int src = sm_perm[k];
+    if (src < 0) break;
+    float x = sm_wsp[k] * __ldg(row + src) - sm_mu[k];
+#pragma unroll
+    for (int c = 0; c < kNPC; ++c) pr[c] = fmaf(x, sm_pc[c * p.LP + k], pr[c]);
+  }
+}
+
+__global__ void __launch_bounds__(256) proj_minmax_kernel(const OrderParams p) {
+  __shared__ float sm_mu[kMaxLP], sm_wsp[kMaxLP], sm_pc[kNPC * kMaxLP];
+  __shared__ int sm_perm[kMaxLP];
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    sm_perm[k] = p.perm[k];
+    sm_wsp[k] = p.wsp[k];
+    sm_mu[k] = p.perm[k] >= 0 ? float(p.mean[p.perm[k]]) : 0.0f;
+  }
+  for (uint32_t e = threadIdx.x; e < kNPC * p.LP; e += blockDim.x) sm_pc[e] = p.pcs[e];
+  __syncthreads();
+  float lo[kNPC], hi[kNPC];
+#pragma unroll
+  for (int c = 0; c < kNPC; ++c) { lo[c] = 3.0e38f; hi[c] = -3.0e38f; }
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.N; i += uint64_t(gridDim.x) * blockDim.x) {
+    float pr[kNPC];
+    project(p, i, sm_mu, sm_pc, sm_perm, sm_wsp, pr);
+#pragma unroll
+    for (int c = 0; c < kNPC; ++c) { lo[c] = fminf(lo[c], pr[c]); hi[c] = fmaxf(hi[c], pr[c]); }
+  }
+#pragma unroll
+  for (int c = 0; c < kNPC; ++c) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(p.pminmax + 2 * c, f2ord(lo[c]));
+      atomicMax(p.pminmax + 2 * c + 1, f2ord(hi[c]));
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long spread4(unsigned long long x) {
+  // insert 3 zero bits between the low 15 bits of x (4-D Morton)
+  unsigned long long r = 0;
+#pragma unroll
+  for (int b = 0; b < 15; ++b) r |= ((x >> b) & 1ull) << (4 * b);
+  return r;
+}
+
+__global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
+  __shared__ float sm_mu[kMaxLP], sm_wsp[kMaxLP], sm_pc[kNPC * kMaxLP];
+  __shared__ int sm_perm[kMaxLP];
+  __shared__ float sm_lo[kNPC], sm_scale;
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    sm_perm[k] = p.perm[k];
+    sm_wsp[k] = p.wsp[k];
+    sm_mu[k] = p.perm[k] >= 0 ? float(p.mean[p.perm[k]]) : 0.0f;
+  }
+  for (uint32_t e = threadIdx.x; e < kNPC * p.LP; e += blockDim.x) sm_pc[e] = p.pcs[e];
+  if (threadIdx.x == 0) {
+    float rng = 0.0f;
+    for (int c = 0; c < kNPC; ++c) {
+      sm_lo[c] = ord2f(p.pminmax[2 * c]);
+      rng = fmaxf(rng, ord2f(p.pminmax[2 * c + 1]) - sm_lo[c]);
+    }
+    sm_scale = rng > 0.0f ? 32767.0f / rng : 0.0f;  // isotropic grid, 15 bits on the widest axis
+  }
+  __syncthreads();
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.N; i += uint64_t(gridDim.x) * blockDim.x) {
+    float pr[kNPC];
+    project(p, i, sm_mu, sm_pc, sm_perm, sm_wsp, pr);
+    unsigned long long key = 0;
+#pragma unroll
+    for (int c = 0; c < kNPC; ++c) {
+      float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sm_scale, 0.0f), 32767.0f);
+      key |= spread4((unsigned long long)q) << c;
+    }
+    p.keys[i] = key;
+    p.vals[i] = uint32_t(i);
+  }
+}
+
+// ---- scan-order copy: bankp[j][k] = -(wsp[k] * bank[order[j]][perm[k]]), idxmap[j] = order[j] ----
+__global__ void __launch_bounds__(256) permute_kernel(const OrderParams p) {
+  __shared__ int sperm[kMaxLP];
+  __shared__ float swsp[kMaxLP];
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    sperm[k] = p.perm[k];
+    swsp[k] = p.wsp[k];
+  }
+  __syncthreads();
+  uint64_t total = p.N * p.LP;
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t j = e / p.LP;
+    uint32_t k = uint32_t(e - j * p.LP);
+    uint64_t i = p.order ? p.order[j] : j;
+    int src = sperm[k];
+    float v = 0.0f;
+    if (src >= 0) v = -__fmul_rn(swsp[k], __ldg(p.bank + i * p.LS + src));
+    p.bankp[e] = v;
+    if (k == 0 && p.idxmap) p.idxmap[j] = uint32_t(i);
+  }
+}
+
+// ---- tile bounds: per tile of T rows and per frame, min and max of bankp ----
+__global__ void __launch_bounds__(128) tile_bounds_kernel(const OrderParams p) {
+  uint64_t t = blockIdx.x;
+  uint64_t r0 = t * kTile;
+  uint64_t r1 = r0 + kTile < p.N ? r0 + kTile : p.N;
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    float lo = 3.0e38f, hi = -3.0e38f;
+    for (uint64_t j = r0; j < r1; ++j) {
+      float v = p.bankp[j * p.LP + k];
+      lo = fminf(lo, v);
+      hi = fmaxf(hi, v);
+    }
+    p.tbounds[(t * 2 + 0) * p.LP + k] = lo;
+    p.tbounds[(t * 2 + 1) * p.LP + k] = hi;
+  }
+}
+
+__global__ void __launch_bounds__(128) super_bounds_kernel(const OrderParams p, uint64_t ntile) {
+  uint64_t s = blockIdx.x;
+  uint64_t t0 = s * kSuper;
+  uint64_t t1 = t0 + kSuper < ntile ? t0 + kSuper : ntile;
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    float lo = 3.0e38f, hi = -3.0e38f;
+    for (uint64_t t = t0; t < t1; ++t) {
+      lo = fminf(lo, p.tbounds[(t * 2 + 0) * p.LP + k]);
+      hi = fmaxf(hi, p.tbounds[(t * 2 + 1) * p.LP + k]);
+    }
+    p.sbounds[(s * 2 + 0) * p.LP + k] = lo;
+    p.sbounds[(s * 2 + 1) * p.LP + k] = hi;
+  }
+}
+
+}  // namespace
+
+size_t order_sort_temp_bytes(uint64_t N) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, int(N), 0, kNPC * 15);
+  return bytes;
+}
+
+cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launches) {
+  frame_stats_kernel<<<p.L, 256, 0, st>>>(p);
+  frame_perm_kernel<<<1, 32, 0, st>>>(p);
+  *launches += 2;
+  OrderParams q = p;
+  if (p.tree) {
+    cudaMemsetAsync(p.cov, 0, sizeof(double) * p.LP * p.LP, st);
+    cov_kernel<<<dim3(p.LP, p.LP), 256, 0, st>>>(p);
+    pca_kernel<<<1, 128, 0, st>>>(p);
+    unsigned int init[2 * kNPC];
+    for (int c = 0; c < kNPC; ++c) {
+      init[2 * c] = 0xffffffffu;
+      init[2 * c + 1] = 0u;
+    }
+    cudaMemcpyAsync(p.pminmax, init, sizeof init, cudaMemcpyHostToDevice, st);
+    proj_minmax_kernel<<<148 * 4, 256, 0, st>>>(p);
+    key_kernel<<<148 * 8, 256, 0, st>>>(p);
+    *launches += 4;
+    size_t tb = p.sort_temp_bytes;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(p.sort_temp, tb, p.keys, p.keys_alt, p.vals, p.order, int(p.N), 0,
+                                                    kNPC * 15, st);
+    if (e != cudaSuccess) return e;
+    *launches += 4;  // onesweep: histogram + passes (approximate count of CUB launches)
+  } else {
+    q.order = nullptr;
+  }
+  permute_kernel<<<148 * 8, 256, 0, st>>>(q);
+  *launches += 1;
+  if (p.tree) {
+    uint64_t ntile = (p.N + kTile - 1) / kTile;
+    uint64_t nsup = (ntile + kSuper - 1) / kSuper;
+    tile_bounds_kernel<<<unsigned(ntile), 128, 0, st>>>(p);
+    super_bounds_kernel<<<unsigned(nsup), 128, 0, st>>>(p, ntile);
+    *launches += 2;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace vpet

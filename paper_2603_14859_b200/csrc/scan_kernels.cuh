@@ -1,0 +1,585 @@
+// scan_kernels.cuh -- K2: the FP32 pass of Alg. 1 lines 4-5, fused distance +
+// per-voxel selection.  Included by scan_wl2.cu / scan_l1.cu (one distance each).
+//
+// One thread owns R voxels; their prescaled TACs (y~_k = wsp_k * y_perm(k)) live in registers as
+// float2 pairs.  The CTA streams tiles of the negated, prescaled, scan-order bank
+// (bankp[j][k] = -wsp_k s_{i(j), perm(k)}) through a 4-stage shared-memory ring filled by
+// cp.async.bulk (TMA bulk copies completing on mbarriers).  For every draw and voxel:
+//     d = y~ + bankp_j          (FADD2: two frames per instruction)
+//     acc = fma(d, d, acc)      (FFMA2, WL2)     or    acc += |d|   (L1)
+// Frames are visited in descending-spread order; after every chunk of CH frames the warp drops
+// the draw if no lane's partial sum is below its threshold (prefix sums of non-negative terms
+// are monotone under rounding, so this is exact).
+//
+// Two variants:
+//   scan_flat_kernel  draws in index order, every tile of the bank (ABC_FLAG_NO_TREE).
+//   scan_tree_kernel  draws in Morton order of their principal-axis projections (order.cu);
+//                     per tile and per super-tile of ST tiles the per-frame [min, max] of bankp
+//                     gives, with the same FP32 chain, a lower bound LB32 <= D32 of every draw
+//                     inside (|fl(y + b)| >= gap by monotone rounding), so a (super-)tile whose
+//                     LB32 >= threshold for all lanes of a warp is skipped by that warp, and one
+//                     skipped by all warps is never loaded.  Each warp first scans the super-tile
+//                     closest to its mean TAC (seeding) so thresholds drop early.
+// Top-n mode keeps the K = n + slack smallest (D32, i) keys per voxel in a global max-heap and K3
+// re-scores them in FP64; eps mode re-scores every draw with D32 <= eps + err(eps) inline.
+#pragma once
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace vpet {
+namespace scan {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int NST = 4;
+constexpr int CH = 8;
+constexpr int T = kTile;
+
+template <int LP>
+struct Shape {
+  static constexpr int R = (LP <= 48) ? 2 : 1;
+  static constexpr int MINB = (LP * R <= 96) ? 2 : 1;
+  static constexpr size_t STAGE_FLOATS = size_t(T) * LP;
+  static constexpr size_t SMEM = size_t(NST) * (STAGE_FLOATS * 4 + T * 4) + NST * 8 + NST * 4 +
+                                 NW * 4 + NW * 4 + NW * LP * 4 + 64;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Max-heap of K keys (D32 bits << 32 | draw index) per voxel, in global memory.  A key above
+// the root of a full heap is ignored.  Returns (new count, new threshold bits).
+static __device__ __noinline__ uint2 heap_push(unsigned long long* h, uint32_t K, uint32_t cnt, unsigned long long key) {
+  if (cnt < K) {
+    uint32_t pos = cnt++;
+    while (pos > 0) {
+      uint32_t par = (pos - 1) >> 1;
+      unsigned long long pk = h[par];
+      if (pk >= key) break;
+      h[pos] = pk;
+      pos = par;
+    }
+    h[pos] = key;
+  } else if (key < h[0]) {
+    uint32_t pos = 0;
+    for (;;) {
+      uint32_t l = 2 * pos + 1;
+      if (l >= K) break;
+      uint32_t c = l;
+      unsigned long long hc = h[l];
+      if (l + 1 < K) {
+        unsigned long long hr = h[l + 1];
+        if (hr > hc) { c = l + 1; hc = hr; }
+      }
+      if (hc <= key) break;
+      h[pos] = hc;
+      pos = c;
+    }
+    h[pos] = key;
+  }
+  float tau = (cnt >= K) ? __uint_as_float(uint32_t(h[0] >> 32)) : __int_as_float(0x7f800000);
+  return make_uint2(cnt, __float_as_uint(tau));
+}
+
+// Exact FP64 discrepancy in acquisition order, operation for operation as the oracle.
+__device__ __forceinline__ double exact_distance(const float* y, const float* s, const float* w, uint32_t L,
+                                                 int dist) {
+  double D = 0.0;
+  for (uint32_t f = 0; f < L; ++f) {
+    double d = __dsub_rn(double(y[f]), double(__ldg(s + f)));
+    double t = (dist == ABC_DIST_L1) ? fabs(d) : __dmul_rn(d, d);
+    D = __dadd_rn(D, __dmul_rn(double(__ldg(w + f)), t));
+  }
+  return D;
+}
+
+// Eps mode: exact re-score of a candidate; accepted draws update the voxel's moment sums.
+static __device__ __noinline__ void eps_candidate(const float* yrow, const float* bank, uint32_t LS, const float* w,
+                                           uint32_t L, int dist, double eps, double* mom, const PriorDev* prior,
+                                           uint64_t i) {
+  double D = exact_distance(yrow, bank + i * LS, w, L, dist);
+  if (!(D <= eps)) return;
+  float th[ABC_MAX_P];
+  int m = draw_theta(*prior, i, th);
+  const ModelDev& md = prior->m[m];
+  double* s = mom + size_t(m) * MOMW;
+  s[0] += 1.0;
+  for (uint32_t k = 0; k < md.P; ++k) {
+    double x = double(th[k]) - double(md.lo[k]);
+    s[1 + 2 * k] += x;
+    s[2 + 2 * k] += x * x;
+  }
+  if (md.kind <= ABC_2TCM_REV) {
+    double ki = double(th[0]) * double(th[2]) / (double(th[1]) + double(th[2]));
+    s[1 + 2 * ABC_MAX_P] += ki;
+    s[2 + 2 * ABC_MAX_P] += ki * ki;
+  }
+}
+
+// Per-thread voxel state.
+template <int LP, int R>
+struct Voxels {
+  float2 y[R][LP / 2];
+  float tau[R], tp[R];
+  uint32_t cnt[R];
+  uint64_t vox[R];
+};
+
+template <int LP, int R>
+__device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& V, int tid) {
+  const float INF = __int_as_float(0x7f800000);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    uint64_t v = uint64_t(blockIdx.x) * (NT * R) + uint64_t(r) * NT + tid;
+    V.vox[r] = v;
+    bool valid = v < p.J;
+    const float* yr = p.tacs + (valid ? v : 0) * p.L;
+#pragma unroll
+    for (int k = 0; k < LP; k += 2) {
+      int s0 = __ldg(p.perm + k), s1 = __ldg(p.perm + k + 1);
+      float a = (valid && s0 >= 0) ? __fmul_rn(__ldg(p.wsp + k), __ldg(yr + s0)) : 0.0f;
+      float b = (valid && s1 >= 0) ? __fmul_rn(__ldg(p.wsp + k + 1), __ldg(yr + s1)) : 0.0f;
+      V.y[r][k / 2] = make_float2(a, b);
+    }
+    V.cnt[r] = 0;
+    if (!p.eps_mode) {
+      V.tau[r] = valid ? INF : -INF;
+    } else {
+      double Y2 = 0.0, Y1 = 0.0;
+      if (valid) {
+        for (uint32_t f = 0; f < p.L; ++f) {
+          double yv = yr[f], wv = __ldg(p.w + f);
+          Y2 += wv * yv * yv;
+          Y1 += wv * fabs(yv);
+        }
+      }
+      double err = p.eb.a * p.eps + p.eb.b * sqrt(Y2 * p.eps) + p.eb.c * Y2 + p.eb.d * Y1;
+      // candidates: D32 <= eps + err(eps)  <=>  D32 < next float above it
+      V.tau[r] = valid ? nextafterf(__double2float_ru(p.eps + err), INF) : -INF;
+    }
+    V.tp[r] = (p.prune || !valid) ? V.tau[r] : INF;
+  }
+}
+
+// Chunk [c*CH, min((c+1)*CH, LP)) of the distance of R voxels to one bank row (scan order).
+template <int LP, int R, int DIST, int C>
+__device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const float* sr, float2 (&acc)[R]) {
+#pragma unroll
+  for (int q = C * CH; q < ((C + 1) * CH < LP ? (C + 1) * CH : LP); q += 4) {
+    const float4 s4 = *reinterpret_cast<const float4*>(sr + q);
+    const float2 sa = make_float2(s4.x, s4.y);
+    const float2 sc = make_float2(s4.z, s4.w);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float2 d0 = __fadd2_rn(V.y[r][q / 2], sa);
+      float2 d1 = __fadd2_rn(V.y[r][q / 2 + 1], sc);
+      if (DIST == ABC_DIST_WL2) {
+        acc[r] = __ffma2_rn(d0, d0, acc[r]);
+        acc[r] = __ffma2_rn(d1, d1, acc[r]);
+      } else {
+        acc[r].x = __fadd_rn(acc[r].x, fabsf(d0.x));
+        acc[r].y = __fadd_rn(acc[r].y, fabsf(d0.y));
+        acc[r].x = __fadd_rn(acc[r].x, fabsf(d1.x));
+        acc[r].y = __fadd_rn(acc[r].y, fabsf(d1.y));
+      }
+    }
+  }
+}
+
+// Same chunk of the lower bound against a box [lo, hi] of bankp values (global memory).
+template <int LP, int R, int DIST, int C>
+__device__ __forceinline__ void bound_chunk(const Voxels<LP, R>& V, const float* lo, const float* hi,
+                                            float2 (&acc)[R]) {
+#pragma unroll
+  for (int q = C * CH; q < ((C + 1) * CH < LP ? (C + 1) * CH : LP); q += 4) {
+    const float4 l4 = __ldg(reinterpret_cast<const float4*>(lo + q));
+    const float4 h4 = __ldg(reinterpret_cast<const float4*>(hi + q));
+    const float2 la = make_float2(l4.x, l4.y), lc = make_float2(l4.z, l4.w);
+    const float2 ha = make_float2(h4.x, h4.y), hc = make_float2(h4.z, h4.w);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      // d = fl(y + b) for b in [lo, hi]:  fl(y + lo) <= d <= fl(y + hi)  =>  |d| >= gap
+      float2 a0 = __fadd2_rn(V.y[r][q / 2], la), b0 = __fadd2_rn(V.y[r][q / 2], ha);
+      float2 a1 = __fadd2_rn(V.y[r][q / 2 + 1], lc), b1 = __fadd2_rn(V.y[r][q / 2 + 1], hc);
+      float2 g0 = make_float2(fmaxf(fmaxf(a0.x, -b0.x), 0.0f), fmaxf(fmaxf(a0.y, -b0.y), 0.0f));
+      float2 g1 = make_float2(fmaxf(fmaxf(a1.x, -b1.x), 0.0f), fmaxf(fmaxf(a1.y, -b1.y), 0.0f));
+      if (DIST == ABC_DIST_WL2) {
+        acc[r] = __ffma2_rn(g0, g0, acc[r]);
+        acc[r] = __ffma2_rn(g1, g1, acc[r]);
+      } else {
+        acc[r].x = __fadd_rn(acc[r].x, g0.x);
+        acc[r].y = __fadd_rn(acc[r].y, g0.y);
+        acc[r].x = __fadd_rn(acc[r].x, g1.x);
+        acc[r].y = __fadd_rn(acc[r].y, g1.y);
+      }
+    }
+  }
+}
+
+template <int LP, int R>
+__device__ __forceinline__ bool any_alive(const Voxels<LP, R>& V, const float2 (&acc)[R]) {
+  bool alive = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) alive |= (__fadd_rn(acc[r].x, acc[r].y) < V.tp[r]);
+  return __any_sync(0xffffffffu, alive);
+}
+
+// Unrolled chunk loop with warp-uniform early exit after each chunk.
+template <int LP, int R, int DIST, bool BOUND, int C>
+struct Chunks {
+  static constexpr int NCH = (LP + CH - 1) / CH;
+  __device__ __forceinline__ static bool run(const Voxels<LP, R>& V, const float* a, const float* b, float2 (&acc)[R],
+                                             unsigned long long& work) {
+    if (BOUND) bound_chunk<LP, R, DIST, C>(V, a, b, acc);
+    else dist_chunk<LP, R, DIST, C>(V, a, acc);
+    work += uint64_t(((C + 1) * CH < LP ? (C + 1) * CH : LP) - C * CH) * R;
+    if (!any_alive<LP, R>(V, acc)) return false;
+    if constexpr (C + 1 < NCH) return Chunks<LP, R, DIST, BOUND, C + 1>::run(V, a, b, acc, work);
+    return true;
+  }
+};
+
+// Evaluate one bank row (scan order) against the thread's voxels; insert survivors.
+template <int LP, int R, int DIST, bool COUNT>
+__device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, const float* sr, uint64_t i,
+                                         unsigned long long& work) {
+  float2 acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
+  unsigned long long w = 0;
+  bool go = Chunks<LP, R, DIST, false, 0>::run(V, sr, nullptr, acc, w);
+  if (COUNT) work += w;
+  if (go) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float D = __fadd_rn(acc[r].x, acc[r].y);
+      if (D < V.tau[r]) {
+        if (!p.eps_mode) {
+          unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
+          uint2 st = heap_push(p.heap + V.vox[r] * p.K, p.K, V.cnt[r], key);
+          V.cnt[r] = st.x;
+          V.tau[r] = __uint_as_float(st.y);
+          if (p.prune) V.tp[r] = V.tau[r];
+        } else {
+          eps_candidate(p.tacs + V.vox[r] * p.L, p.bank, p.LS, p.w, p.L, p.dist, p.eps,
+                        p.mom + V.vox[r] * (size_t(p.M) * MOMW), p.prior_g, i);
+        }
+      }
+    }
+  }
+}
+
+template <int LP, int R, int DIST>
+__device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const float* box, unsigned long long& work) {
+  float2 acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
+  return Chunks<LP, R, DIST, true, 0>::run(V, box, box + LP, acc, work);
+}
+
+template <int LP, int R>
+__device__ __forceinline__ void finish(const ScanParams& p, const Voxels<LP, R>& V, unsigned long long work,
+                                       unsigned long long bwork, int lane, bool count) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (V.vox[r] < p.J && !p.eps_mode) p.heap_cnt[V.vox[r]] = V.cnt[r];
+  if (count) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      work += __shfl_xor_sync(0xffffffffu, work, o);
+      bwork += __shfl_xor_sync(0xffffffffu, bwork, o);
+    }
+    if (lane == 0) {
+      atomicAdd(p.work, work);
+      if (p.bound_work) atomicAdd(p.bound_work, bwork);
+    }
+  }
+}
+
+// =============================================================================================
+// Flat scan: every tile, index order (ABC_FLAG_NO_TREE, and N >= 2^31).
+// =============================================================================================
+template <int LP, int DIST, bool COUNT>
+__global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_flat_kernel(const ScanParams p) {
+  constexpr int R = Shape<LP>::R;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage = reinterpret_cast<float*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NST * (Shape<LP>::STAGE_FLOATS * 4 + T * 4));
+  int* arrivals = reinterpret_cast<int*>(full + NST);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t N = p.N;
+  const uint32_t ntile = uint32_t((N + T - 1) / T);
+  const float* __restrict__ bankp = p.bankp;
+  auto issue = [=](uint32_t tt, int ss) {
+    uint64_t i0 = uint64_t(tt) * T;
+    uint32_t nd = uint32_t((N - i0) < uint64_t(T) ? (N - i0) : uint64_t(T));
+    mbar_expect_tx(&full[ss], nd * LP * 4u);
+    bulk_g2s(stage + size_t(ss) * Shape<LP>::STAGE_FLOATS, bankp + i0 * LP, nd * LP * 4u, &full[ss]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      arrivals[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (uint32_t s = 0; s < uint32_t(NST) && s < ntile; ++s) issue(s, int(s));
+  Voxels<LP, R> V;
+  load_voxels<LP, R>(p, V, tid);
+  unsigned long long work = 0;
+  for (uint32_t t = 0; t < ntile; ++t) {
+    const int s = int(t % NST);
+    mbar_wait(&full[s], (t / NST) & 1u);
+    const float* sb = stage + size_t(s) * Shape<LP>::STAGE_FLOATS;
+    const uint64_t rem = N - uint64_t(t) * T;
+    const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
+    const uint64_t ibase = uint64_t(t) * T;
+    for (uint32_t d = 0; d < nd; ++d) eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, ibase + d, work);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      int old = atomicAdd(&arrivals[s], 1);
+      if (old == NW - 1) {
+        atomicExch(&arrivals[s], 0);
+        uint32_t tn = t + NST;
+        if (tn < ntile) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(tn, s);
+        }
+      }
+    }
+  }
+  finish<LP, R>(p, V, work, 0ull, lane, COUNT);
+}
+
+// =============================================================================================
+// Tree scan: Morton-ordered bank, super-tile / tile bounds, seeding.
+// =============================================================================================
+template <int LP, int DIST, bool COUNT>
+__global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const ScanParams p) {
+  constexpr int R = Shape<LP>::R;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage = reinterpret_cast<float*>(smem_raw);
+  uint32_t* sidx = reinterpret_cast<uint32_t*>(smem_raw + NST * Shape<LP>::STAGE_FLOATS * 4);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NST * (Shape<LP>::STAGE_FLOATS * 4 + T * 4));
+  int* arrivals = reinterpret_cast<int*>(full + NST);
+  uint32_t* wmask = reinterpret_cast<uint32_t*>(arrivals + NST);
+  int* seeds = reinterpret_cast<int*>(wmask + NW);
+  float* ybar = reinterpret_cast<float*>(seeds + NW);
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t N = p.N;
+  const float* __restrict__ bankp = p.bankp;
+  const uint32_t* __restrict__ idxmap = p.idxmap;
+  auto issue = [=](uint64_t tt, int ss) {
+    uint64_t i0 = tt * T;
+    uint32_t nd = uint32_t((N - i0) < uint64_t(T) ? (N - i0) : uint64_t(T));
+    uint32_t ndp = (nd + 3u) & ~3u;  // idxmap is padded to a multiple of 4 entries (16-B copies)
+    mbar_expect_tx(&full[ss], nd * LP * 4u + ndp * 4u);
+    bulk_g2s(stage + size_t(ss) * Shape<LP>::STAGE_FLOATS, bankp + i0 * LP, nd * LP * 4u, &full[ss]);
+    bulk_g2s(sidx + ss * T, idxmap + i0, ndp * 4u, &full[ss]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      arrivals[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  Voxels<LP, R> V;
+  load_voxels<LP, R>(p, V, tid);
+
+  // ---- seeding: each warp scans first the super-tile nearest to its mean prescaled TAC ----
+  {
+    int nvalid = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) nvalid += (V.vox[r] < p.J);
+    nvalid = __reduce_add_sync(0xffffffffu, nvalid);
+    float inv = nvalid > 0 ? 1.0f / float(nvalid) : 0.0f;
+#pragma unroll
+    for (int k = 0; k < LP / 2; ++k) {
+      float2 s = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (V.vox[r] < p.J) { s.x += V.y[r][k].x; s.y += V.y[r][k].y; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+      }
+      if (lane == 0) {
+        ybar[wid * LP + 2 * k] = s.x * inv;
+        ybar[wid * LP + 2 * k + 1] = s.y * inv;
+      }
+    }
+    __syncwarp();
+    float best = __int_as_float(0x7f800000);
+    int bi = 0;
+    for (uint64_t s = lane; s < p.nsuper; s += 32) {
+      const float* lo = p.sbounds + s * 2 * LP;
+      const float* hi = lo + LP;
+      float lb = 0.0f;
+      for (int k = 0; k < LP; ++k) {
+        float yk = ybar[wid * LP + k];
+        float g = fmaxf(fmaxf(yk + __ldg(lo + k), -(yk + __ldg(hi + k))), 0.0f);
+        lb = fmaf(g, g, lb);
+        if (lb >= best) break;
+      }
+      if (lb < best) { best = lb; bi = int(s); }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) seeds[wid] = nvalid > 0 ? bi : -1;
+  }
+  __syncthreads();
+  if (tid == 0) {  // drop duplicate seeds (several warps may share their nearest super-tile)
+    for (int w = 1; w < NW; ++w)
+      for (int u = 0; u < w; ++u)
+        if (seeds[w] >= 0 && seeds[u] == seeds[w]) seeds[w] = -1;
+  }
+  __syncthreads();
+
+  unsigned long long work = 0, bwork = 0;
+  uint32_t consumed = 0;
+  const int64_t nsup = int64_t(p.nsuper);
+  for (int64_t it = -NW; it < nsup; ++it) {
+    int64_t s;
+    if (it < 0) {
+      s = seeds[it + NW];
+      if (s < 0) continue;
+    } else {
+      s = it;
+      bool is_seed = false;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) is_seed |= (seeds[w] == s);
+      if (is_seed) continue;
+    }
+    // super-tile bound
+    bool alive = box_alive<LP, R, DIST>(V, p.sbounds + uint64_t(s) * 2 * LP, bwork);
+    if (!__syncthreads_or(alive)) continue;
+    // tile bounds -> per-warp masks
+    const uint64_t t0 = uint64_t(s) * kSuper;
+    const uint64_t t1 = (t0 + kSuper < p.ntile) ? t0 + kSuper : p.ntile;
+    uint32_t mask = 0;
+    if (alive) {
+      for (uint64_t t = t0; t < t1; ++t)
+        if (box_alive<LP, R, DIST>(V, p.tbounds + t * 2 * LP, bwork)) mask |= 1u << uint32_t(t - t0);
+    }
+    if (lane == 0) wmask[wid] = mask;
+    __syncthreads();
+    uint32_t cm = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) cm |= wmask[w];
+    const uint32_t mym = wmask[wid];
+    const uint32_t nal = __popc(cm);
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      uint32_t m = cm;
+      for (uint32_t q = 0; q < nal && q < uint32_t(NST); ++q) {
+        uint32_t b = __ffs(m) - 1;
+        m &= m - 1;
+        issue(t0 + b, int((consumed + q) % NST));
+      }
+    }
+    uint32_t rest = cm;
+    for (uint32_t q = 0; q < nal; ++q) {
+      const uint32_t b = __ffs(rest) - 1;
+      rest &= rest - 1;
+      const uint64_t t = t0 + b;
+      const uint32_t g = consumed + q;
+      const int st = int(g % NST);
+      // every warp observes every phase of the ring (parity waits are only unambiguous when no
+      // phase is skipped), then only the warps whose lanes can improve evaluate the tile
+      mbar_wait(&full[st], (g / NST) & 1u);
+      if ((mym >> b) & 1u) {
+        const float* sb = stage + size_t(st) * Shape<LP>::STAGE_FLOATS;
+        const uint32_t* si = sidx + st * T;
+        const uint64_t rem = N - t * T;
+        const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
+        for (uint32_t d = 0; d < nd; ++d) eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, si[d], work);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        int old = atomicAdd(&arrivals[st], 1);
+        if (old == NW - 1) {
+          atomicExch(&arrivals[st], 0);
+          if (q + NST < nal) {
+            uint32_t m = rest;  // tiles after q; the (NST-1)-th of them is q + NST
+            for (int k = 0; k < NST - 1; ++k) m &= m - 1;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(t0 + (__ffs(m) - 1), st);
+          }
+        }
+      }
+    }
+    consumed += nal;
+  }
+  finish<LP, R>(p, V, work, bwork, lane, COUNT);
+}
+
+template <int LP, int DIST, bool COUNT, bool TREE>
+cudaError_t launch_one(const ScanParams& p, cudaStream_t st) {
+  using S = Shape<LP>;
+  auto kern = TREE ? scan_tree_kernel<LP, DIST, COUNT> : scan_flat_kernel<LP, DIST, COUNT>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  uint64_t per_cta = uint64_t(NT) * S::R;
+  unsigned grid = unsigned((p.J + per_cta - 1) / per_cta);
+  kern<<<grid, NT, S::SMEM, st>>>(p);
+  return cudaGetLastError();
+}
+
+#define VPET_LP_LIST(X) X(8) X(12) X(16) X(20) X(24) X(28) X(32) X(36) X(40) X(44) X(48) X(56) X(64) X(80) X(96) X(128)
+
+template <int DIST>
+cudaError_t launch_dist(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st) {
+#define X(v)                                                                          \
+  if (LP == v) {                                                                      \
+    if (tree) return count_work ? launch_one<v, DIST, true, true>(p, st) : launch_one<v, DIST, false, true>(p, st); \
+    return count_work ? launch_one<v, DIST, true, false>(p, st) : launch_one<v, DIST, false, false>(p, st);         \
+  }
+  VPET_LP_LIST(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace scan
+}  // namespace vpet

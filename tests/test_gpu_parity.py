@@ -74,9 +74,10 @@ def test_rt_model_selection(rt_small):
     compare(g, o)
 
 
-@pytest.mark.parametrize("flags", [0x2, 0x8, 0x10, 0x8 | 0x10])
-def test_exact_noprune_noreorder_identical(tb_small, flags):
-    """ABC_FLAG_EXACT (pure FP64 scan), NO_PRUNE and NO_REORDER give the same accepted sets."""
+@pytest.mark.parametrize("flags", [0x2, 0x8, 0x10, 0x8 | 0x10, 0x20, 0x20 | 0x8])
+def test_exact_noprune_noreorder_notree_identical(tb_small, flags):
+    """ABC_FLAG_EXACT (pure FP64 scan), NO_PRUNE, NO_REORDER and NO_TREE (flat index-order scan) give
+    bit-identical outputs to the default tree-ordered, bound-pruned FP32 pass."""
     sub = tb_small.subset(np.arange(130))
     base, _ = run_gpu(sub)
     alt, _ = run_gpu(sub, flags=flags)

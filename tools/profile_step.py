@@ -1,0 +1,44 @@
+"""Run the bench workload (config-4 batch, N = 1e7) for a few steps -- the command profiled by ncu.
+
+python tools/profile_step.py --save /tmp/p.pkl            # generate inputs once (RK4 phantom on GPU)
+python tools/profile_step.py --load /tmp/p.pkl --steps 2  # run (no input generation: ncu-friendly)
+"""
+import argparse
+import os
+import pickle
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--max-voxels", type=int, default=None)
+ap.add_argument("--draws", type=int, default=10_000_000)
+ap.add_argument("--flags", type=int, default=0)
+ap.add_argument("--save", default=None)
+ap.add_argument("--load", default=None)
+a = ap.parse_args()
+if a.load:
+    prob = pickle.load(open(a.load, "rb"))
+else:
+    import synthetic as S
+    prob = S.config4_chunk(chunk=0, n_chunks=32, N=a.draws, n=18, device="cuda", max_voxels=a.max_voxels)
+    if a.save:
+        pickle.dump(prob, open(a.save, "wb"))
+        print("saved", a.save, prob.tacs.shape)
+        sys.exit(0)
+from paper_2603_14859_b200 import FLAG_TIMING, AbcContext  # noqa: E402
+
+ctx = AbcContext(**dict(prob.ctx_kwargs, flags=FLAG_TIMING | a.flags))
+prob.setup(ctx)
+y = np.ascontiguousarray(prob.tacs)
+for s in range(a.steps):
+    t = time.time()
+    r = ctx.run_voxels(y)
+    st = ctx.stats()
+    print(f"step {s}: {time.time() - t:.3f} s  scan {st['ms_scan']:.1f} ms  order {st['ms_order']:.1f} ms  "
+          f"bank {st['ms_bank']:.1f} ms  certify {st['ms_certify']:.2f} ms  fallback voxels {st['n_fallback']}  "
+          f"launches {st['gpu_launches']}", flush=True)
