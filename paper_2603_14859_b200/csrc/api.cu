@@ -78,7 +78,7 @@ struct abc_ctx {
   DevBuf d_fdur, d_fs, d_fe, d_favg, d_w, d_wsc, d_gt, d_gc, d_gframe, d_ft, d_fc, d_fframe;
   // work buffers
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
-  DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds;
+  DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, tau_glob, queue;
   abc_stats stats{};
   bool bank_valid = false;
   bool dist_wl2() const { return cfg.distance == ABC_DIST_WL2; }
@@ -488,8 +488,15 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const bool tree = !exact && !(ctx->cfg.flags & ABC_FLAG_NO_TREE) && N < (1ull << 31);
   const uint64_t ntile = (N + kTile - 1) / kTile, nsuper = (ntile + kSuper - 1) / kSuper;
   const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
+  // draw-range split of the tree scan (interleaved super-tiles): balances heavy voxels over SMs
+  uint32_t nparts = 1;
+  if (tree && !eps) nparts = K <= 64 ? 8u : (K <= 512 ? 2u : 1u);
+  if (tree && eps) nparts = 8u;
+  if (nparts > nsuper) nparts = uint32_t(nsuper);
+  if (nparts == 0) nparts = 1;
   if (tree) need += N * (8 + 8 + 4 + 4 + 4) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper);
-  if (!eps) need += size_t(8) * J * K + 4 * J;           // heaps
+  if (!eps) need += (size_t(8) * K + 4) * J * (nparts - 1) + 4 * J;
+  if (!eps) need += size_t(8) * J * K + 4 * J;           // heaps (x nparts in tree mode, below)
   need += size_t(12) * J * (n ? n : 1);                  // exact heaps (fallback)
   if (eps) need += sizeof(double) * J * M * MOMW;
   if (host_tacs) need += sizeof(float) * J * L;
@@ -516,12 +523,14 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(ctx->sort_temp.ensure(sort_tmp));
     CK(ctx->tbounds.ensure(sizeof(float) * 2 * LP * ntile));
     CK(ctx->sbounds.ensure(sizeof(float) * 2 * LP * nsuper));
+    CK(ctx->tau_glob.ensure(4 * J));
+    CK(ctx->queue.ensure(16));
   }
   CK(ctx->perm.ensure(sizeof(int) * kMaxLP));
   CK(ctx->wsp.ensure(sizeof(float) * kMaxLP));
   if (!eps) {
-    CK(ctx->heap.ensure(size_t(8) * J * std::max<uint32_t>(K, 1)));
-    CK(ctx->heap_cnt.ensure(4 * J));
+    CK(ctx->heap.ensure(size_t(8) * J * nparts * std::max<uint32_t>(K, 1)));
+    CK(ctx->heap_cnt.ensure(4 * J * nparts));
     CK(ctx->hd.ensure(sizeof(double) * J * n));
     CK(ctx->hidx.ensure(sizeof(uint32_t) * J * n));
   } else {
@@ -649,7 +658,13 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       sp.sbounds = ctx->sbounds.as<float>();
       sp.ntile = ntile;
       sp.nsuper = nsuper;
+      sp.tau_glob = eps ? nullptr : ctx->tau_glob.as<unsigned int>();
+      sp.queue = ctx->queue.as<unsigned int>();
+      if (!eps) launch_fill_u32(ctx->tau_glob.as<uint32_t>(), 0x7f800000u, J, st);
+      CK(cudaMemsetAsync(ctx->queue.p, 0, 16, st));
+      launches += eps ? 0 : 1;
     }
+    sp.nparts = nparts;
     sp.bound_work = ctx->work.as<unsigned long long>() + 1;
     if (eps) CK(cudaMemsetAsync(ctx->mom.p, 0, sizeof(double) * J * M * MOMW, st));
     CK(ctx->dist_wl2() ? launch_scan_wl2(sp, LP, count_work, tree, st) : launch_scan_l1(sp, LP, count_work, tree, st));
@@ -659,6 +674,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
 
   ReduceParams rp{};
   rp.K = K;
+  rp.nparts = (tree && !eps) ? nparts : 1;
+  rp.tau_glob = (tree && !eps) ? ctx->tau_glob.as<unsigned int>() : nullptr;
   rp.heap = ctx->heap.as<unsigned long long>();
   rp.heap_cnt = ctx->heap_cnt.as<uint32_t>();
   rp.hd = ctx->hd.as<double>();
@@ -795,7 +812,8 @@ void abc_destroy(abc_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs2[] = {&ctx->fmean, &ctx->cov, &ctx->pcs, &ctx->pminmax, &ctx->keys, &ctx->keys_alt, &ctx->vals,
-                     &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds};
+                     &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->tau_glob,
+                     &ctx->queue};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,

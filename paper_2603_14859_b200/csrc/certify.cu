@@ -196,7 +196,7 @@ __global__ void certify_reduce_kernel(const ReduceParams p, uint32_t Kp, uint32_
     const uint64_t v = p.list ? p.list[e] : e;
     const float* y = p.tacs + v * p.L;
     uint32_t cnt;
-    float tK = 0.0f;
+    float tK = __int_as_float(0x7f800000);
     if (p.exact) {
       cnt = p.n;
       for (uint32_t a = lane; a < Kp; a += 32) {
@@ -204,32 +204,62 @@ __global__ void certify_reduce_kernel(const ReduceParams p, uint32_t Kp, uint32_
         ci[a] = a < cnt ? p.hidx[v * p.n + a] : 0xffffffffu;
       }
     } else {
-      cnt = p.heap_cnt[v];
-      const uint32_t need = uint32_t(uint64_t(p.K) < p.N ? uint64_t(p.K) : p.N);
-      if (cnt < need) {  // heap never filled (non-finite FP32 distances): exact path
+      // Candidates: the keys of all parts' heaps with D32 <= B, where B bounds the D32 of every
+      // draw the FP32 pass excluded (tau_glob in tree mode, the heap root in flat mode).
+      const uint32_t S = p.nparts;
+      float B = __int_as_float(0x7f800000);
+      uint64_t total = 0;
+      for (uint32_t q = 0; q < S; ++q) total += p.heap_cnt[v * S + q];
+      if (p.tau_glob) {
+        B = __uint_as_float(p.tau_glob[v]);
+      } else if (p.heap_cnt[v] >= p.K) {
+        float tmax = 0.0f;
+        for (uint32_t a = lane; a < p.K; a += 32)
+          tmax = fmaxf(tmax, __uint_as_float(uint32_t(p.heap[v * p.K + a] >> 32)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        B = tmax;
+      }
+      const bool complete = (total == p.N);  // every draw was kept: nothing excluded
+      if (!complete && !(B < __int_as_float(0x7f800000))) {  // no finite bound (non-finite D32s)
         if (lane == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
         continue;
       }
-      float tmax = 0.0f;
+      uint32_t nc = 0;  // warp-uniform candidate count
+      for (uint32_t q = 0; q < S; ++q) {
+        const uint32_t cq = p.heap_cnt[v * S + q];
+        const unsigned long long* h = p.heap + (v * S + q) * p.K;
+        for (uint32_t base = 0; base < cq; base += 32) {
+          uint32_t a = base + lane;
+          unsigned long long key = a < cq ? h[a] : ~0ull;
+          bool take = a < cq && __uint_as_float(uint32_t(key >> 32)) <= B;
+          uint32_t bal = __ballot_sync(0xffffffffu, take);
+          if (take) {
+            uint32_t pos = nc + __popc(bal & ((1u << lane) - 1u));
+            if (pos < Kp) ci[pos] = uint32_t(key & 0xffffffffull);
+          }
+          nc += __popc(bal);
+        }
+      }
+      if (nc > Kp || nc < p.n) {  // capacity (or a degenerate bound): exact path
+        if (lane == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+        continue;
+      }
+      __syncwarp();
       for (uint32_t a = lane; a < Kp; a += 32) {
-        if (a < cnt) {
-          unsigned long long key = p.heap[v * p.K + a];
-          uint32_t idx = uint32_t(key & 0xffffffffull);
-          tmax = fmaxf(tmax, __uint_as_float(uint32_t(key >> 32)));
-          cd[a] = exact_distance_c(y, p.bank + uint64_t(idx) * p.LS, p.w, p.L, p.dist);
-          ci[a] = idx;
+        if (a < nc) {
+          cd[a] = exact_distance_c(y, p.bank + uint64_t(ci[a]) * p.LS, p.w, p.L, p.dist);
         } else {
           cd[a] = DINF;
           ci[a] = 0xffffffffu;
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-      tK = tmax;
+      tK = complete ? __int_as_float(0x7f800000) : B;
+      cnt = nc;
     }
     __syncwarp();
     warp_sort_pairs(cd, ci, Kp, lane);
-    if (!p.exact && uint64_t(p.K) < p.N) {
+    if (!p.exact && tK < __int_as_float(0x7f800000)) {
       double Y2 = 0.0, Y1 = 0.0;
       for (uint32_t f = lane; f < p.L; f += 32) {
         double yv = __ldg(y + f), wv = __ldg(p.w + f);
@@ -368,7 +398,7 @@ uint32_t next_pow2(uint32_t x) {
 }  // namespace
 
 void launch_certify_reduce(const ReduceParams& p, cudaStream_t st) {
-  uint32_t Kp = next_pow2(p.exact ? p.n : (p.K > p.n ? p.K : p.n));
+  uint32_t Kp = next_pow2(p.exact ? p.n : (p.K * p.nparts > p.n ? p.K * p.nparts : p.n));
   if (Kp < 32) Kp = 32;
   uint32_t np2 = next_pow2(p.n);
   if (np2 < 32) np2 = 32;

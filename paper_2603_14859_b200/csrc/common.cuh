@@ -224,6 +224,11 @@ struct ScanParams {
   const float* sbounds;     // [nsuper][2][LP]
   uint64_t ntile, nsuper;
   unsigned long long* bound_work;  // LB frame-evaluation counter (COUNT)
+  // work split: item = (voxel tile, part); part p owns super-tiles s = p (mod nparts) and its own
+  // heap [J][nparts][K]; tau_glob[v] = min over parts of their heap thresholds (shared pruning)
+  uint32_t nparts;
+  unsigned int* tau_glob;   // [J] float bits (positive), atomicMin
+  unsigned int* queue;      // work-queue counter (zeroed per run)
 };
 constexpr int MOMW = 2 + 2 * ABC_MAX_P + 2;  // count, (S1,S2) x P, (KS1, KS2), pad
 cudaError_t launch_scan(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);
@@ -251,9 +256,11 @@ void launch_exact_scan(const ExactParams& p, cudaStream_t st);
 struct ReduceParams {
   // candidates
   int exact;                    // 1: candidates from the exact heap (no certification)
-  const unsigned long long* heap;  // fast mode
-  const uint32_t* heap_cnt;
+  const unsigned long long* heap;  // fast mode: [J][nparts][K]
+  const uint32_t* heap_cnt;        // [J][nparts]
   uint32_t K;
+  uint32_t nparts;
+  const unsigned int* tau_glob;    // [J] (tree mode) or nullptr: bound B on excluded draws' D32
   const double* hd;             // exact mode
   const uint32_t* hidx;
   const uint32_t* list;         // voxel list or nullptr

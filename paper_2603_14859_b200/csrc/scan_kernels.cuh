@@ -42,7 +42,7 @@ struct Shape {
   static constexpr int MINB = (LP * R <= 96) ? 2 : 1;
   static constexpr size_t STAGE_FLOATS = size_t(T) * LP;
   static constexpr size_t SMEM = size_t(NST) * (STAGE_FLOATS * 4 + T * 4) + NST * 8 + NST * 4 +
-                                 NW * 4 + NW * 4 + NW * LP * 4 + 64;
+                                 NW * 4 + NW * 4 + NW * LP * 4 + 16 + 64;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
@@ -129,17 +129,17 @@ static __device__ __noinline__ void eps_candidate(const float* yrow, const float
   float th[ABC_MAX_P];
   int m = draw_theta(*prior, i, th);
   const ModelDev& md = prior->m[m];
-  double* s = mom + size_t(m) * MOMW;
-  s[0] += 1.0;
+  double* s = mom + size_t(m) * MOMW;  // parts of one voxel may run concurrently: atomics
+  atomicAdd(s, 1.0);
   for (uint32_t k = 0; k < md.P; ++k) {
     double x = double(th[k]) - double(md.lo[k]);
-    s[1 + 2 * k] += x;
-    s[2 + 2 * k] += x * x;
+    atomicAdd(s + 1 + 2 * k, x);
+    atomicAdd(s + 2 + 2 * k, x * x);
   }
   if (md.kind <= ABC_2TCM_REV) {
     double ki = double(th[0]) * double(th[2]) / (double(th[1]) + double(th[2]));
-    s[1 + 2 * ABC_MAX_P] += ki;
-    s[2 + 2 * ABC_MAX_P] += ki * ki;
+    atomicAdd(s + 1 + 2 * ABC_MAX_P, ki);
+    atomicAdd(s + 2 + 2 * ABC_MAX_P, ki * ki);
   }
 }
 
@@ -147,17 +147,19 @@ static __device__ __noinline__ void eps_candidate(const float* yrow, const float
 template <int LP, int R>
 struct Voxels {
   float2 y[R][LP / 2];
-  float tau[R], tp[R];
+  float tau[R];   // insertion threshold: min(own heap root, shared tau_glob) (top-n) / eps bound
+  float tp[R];    // pruning threshold (tau, or +inf with ABC_FLAG_NO_PRUNE)
+  float taup[R];  // own (part) heap root, +inf until the heap is full
   uint32_t cnt[R];
   uint64_t vox[R];
 };
 
 template <int LP, int R>
-__device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& V, int tid) {
+__device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& V, int tid, uint64_t vtile) {
   const float INF = __int_as_float(0x7f800000);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    uint64_t v = uint64_t(blockIdx.x) * (NT * R) + uint64_t(r) * NT + tid;
+    uint64_t v = vtile * (NT * R) + uint64_t(r) * NT + tid;
     V.vox[r] = v;
     bool valid = v < p.J;
     const float* yr = p.tacs + (valid ? v : 0) * p.L;
@@ -169,8 +171,10 @@ __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& 
       V.y[r][k / 2] = make_float2(a, b);
     }
     V.cnt[r] = 0;
+    V.taup[r] = INF;
     if (!p.eps_mode) {
       V.tau[r] = valid ? INF : -INF;
+      if (valid && p.tau_glob) V.tau[r] = fminf(V.tau[r], __uint_as_float(__ldcg(p.tau_glob + v)));
     } else {
       double Y2 = 0.0, Y1 = 0.0;
       if (valid) {
@@ -269,7 +273,7 @@ struct Chunks {
 // Evaluate one bank row (scan order) against the thread's voxels; insert survivors.
 template <int LP, int R, int DIST, bool COUNT>
 __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, const float* sr, uint64_t i,
-                                         unsigned long long& work) {
+                                         uint32_t part, unsigned long long& work) {
   float2 acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
@@ -283,15 +287,31 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
       if (D < V.tau[r]) {
         if (!p.eps_mode) {
           unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
-          uint2 st = heap_push(p.heap + V.vox[r] * p.K, p.K, V.cnt[r], key);
+          uint2 st = heap_push(p.heap + (V.vox[r] * p.nparts + part) * p.K, p.K, V.cnt[r], key);
           V.cnt[r] = st.x;
-          V.tau[r] = __uint_as_float(st.y);
+          V.taup[r] = __uint_as_float(st.y);
+          if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + V.vox[r], st.y);
+          V.tau[r] = fminf(V.tau[r], V.taup[r]);
           if (p.prune) V.tp[r] = V.tau[r];
         } else {
           eps_candidate(p.tacs + V.vox[r] * p.L, p.bank, p.LS, p.w, p.L, p.dist, p.eps,
                         p.mom + V.vox[r] * (size_t(p.M) * MOMW), p.prior_g, i);
         }
       }
+    }
+  }
+}
+
+// Pull the other parts' progress on the shared thresholds.
+template <int LP, int R>
+__device__ __forceinline__ void refresh_tau(const ScanParams& p, Voxels<LP, R>& V) {
+  if (p.eps_mode || !p.tau_glob) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (V.vox[r] < p.J) {
+      float g = __uint_as_float(__ldcg(p.tau_glob + V.vox[r]));
+      V.tau[r] = fminf(V.tau[r], g);
+      if (p.prune) V.tp[r] = V.tau[r];
     }
   }
 }
@@ -305,11 +325,14 @@ __device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const float* b
 }
 
 template <int LP, int R>
-__device__ __forceinline__ void finish(const ScanParams& p, const Voxels<LP, R>& V, unsigned long long work,
-                                       unsigned long long bwork, int lane, bool count) {
+__device__ __forceinline__ void store_counts(const ScanParams& p, const Voxels<LP, R>& V, uint32_t part) {
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if (V.vox[r] < p.J && !p.eps_mode) p.heap_cnt[V.vox[r]] = V.cnt[r];
+    if (V.vox[r] < p.J && !p.eps_mode) p.heap_cnt[V.vox[r] * p.nparts + part] = V.cnt[r];
+}
+
+__device__ __forceinline__ void finish_counts(const ScanParams& p, unsigned long long work, unsigned long long bwork,
+                                              int lane, bool count) {
   if (count) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -354,7 +377,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_flat_kernel(const Sc
   if (tid == 0)
     for (uint32_t s = 0; s < uint32_t(NST) && s < ntile; ++s) issue(s, int(s));
   Voxels<LP, R> V;
-  load_voxels<LP, R>(p, V, tid);
+  load_voxels<LP, R>(p, V, tid, blockIdx.x);
   unsigned long long work = 0;
   for (uint32_t t = 0; t < ntile; ++t) {
     const int s = int(t % NST);
@@ -363,7 +386,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_flat_kernel(const Sc
     const uint64_t rem = N - uint64_t(t) * T;
     const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
     const uint64_t ibase = uint64_t(t) * T;
-    for (uint32_t d = 0; d < nd; ++d) eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, ibase + d, work);
+    for (uint32_t d = 0; d < nd; ++d) eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, ibase + d, 0u, work);
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
@@ -378,7 +401,8 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_flat_kernel(const Sc
       }
     }
   }
-  finish<LP, R>(p, V, work, 0ull, lane, COUNT);
+  store_counts<LP, R>(p, V, 0u);
+  finish_counts(p, work, 0ull, lane, COUNT);
 }
 
 // =============================================================================================
@@ -395,6 +419,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
   uint32_t* wmask = reinterpret_cast<uint32_t*>(arrivals + NST);
   int* seeds = reinterpret_cast<int*>(wmask + NW);
   float* ybar = reinterpret_cast<float*>(seeds + NW);
+  int* s_item = reinterpret_cast<int*>(ybar + NW * LP);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t N = p.N;
@@ -415,140 +440,158 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  Voxels<LP, R> V;
-  load_voxels<LP, R>(p, V, tid);
-
-  // ---- seeding: each warp scans first the super-tile nearest to its mean prescaled TAC ----
-  {
-    int nvalid = 0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) nvalid += (V.vox[r] < p.J);
-    nvalid = __reduce_add_sync(0xffffffffu, nvalid);
-    float inv = nvalid > 0 ? 1.0f / float(nvalid) : 0.0f;
-#pragma unroll
-    for (int k = 0; k < LP / 2; ++k) {
-      float2 s = make_float2(0.0f, 0.0f);
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (V.vox[r] < p.J) { s.x += V.y[r][k].x; s.y += V.y[r][k].y; }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
-        s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
-      }
-      if (lane == 0) {
-        ybar[wid * LP + 2 * k] = s.x * inv;
-        ybar[wid * LP + 2 * k + 1] = s.y * inv;
-      }
-    }
-    __syncwarp();
-    float best = __int_as_float(0x7f800000);
-    int bi = 0;
-    for (uint64_t s = lane; s < p.nsuper; s += 32) {
-      const float* lo = p.sbounds + s * 2 * LP;
-      const float* hi = lo + LP;
-      float lb = 0.0f;
-      for (int k = 0; k < LP; ++k) {
-        float yk = ybar[wid * LP + k];
-        float g = fmaxf(fmaxf(yk + __ldg(lo + k), -(yk + __ldg(hi + k))), 0.0f);
-        lb = fmaf(g, g, lb);
-        if (lb >= best) break;
-      }
-      if (lb < best) { best = lb; bi = int(s); }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      float ob = __shfl_xor_sync(0xffffffffu, best, o);
-      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    if (lane == 0) seeds[wid] = nvalid > 0 ? bi : -1;
-  }
-  __syncthreads();
-  if (tid == 0) {  // drop duplicate seeds (several warps may share their nearest super-tile)
-    for (int w = 1; w < NW; ++w)
-      for (int u = 0; u < w; ++u)
-        if (seeds[w] >= 0 && seeds[u] == seeds[w]) seeds[w] = -1;
-  }
-  __syncthreads();
-
+  const uint32_t S = p.nparts;
+  const uint64_t nvt = (p.J + uint64_t(NT) * R - 1) / (uint64_t(NT) * R);
+  const uint64_t nitems = nvt * S;
   unsigned long long work = 0, bwork = 0;
-  uint32_t consumed = 0;
-  const int64_t nsup = int64_t(p.nsuper);
-  for (int64_t it = -NW; it < nsup; ++it) {
-    int64_t s;
-    if (it < 0) {
-      s = seeds[it + NW];
-      if (s < 0) continue;
-    } else {
-      s = it;
-      bool is_seed = false;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) is_seed |= (seeds[w] == s);
-      if (is_seed) continue;
-    }
-    // super-tile bound
-    bool alive = box_alive<LP, R, DIST>(V, p.sbounds + uint64_t(s) * 2 * LP, bwork);
-    if (!__syncthreads_or(alive)) continue;
-    // tile bounds -> per-warp masks
-    const uint64_t t0 = uint64_t(s) * kSuper;
-    const uint64_t t1 = (t0 + kSuper < p.ntile) ? t0 + kSuper : p.ntile;
-    uint32_t mask = 0;
-    if (alive) {
-      for (uint64_t t = t0; t < t1; ++t)
-        if (box_alive<LP, R, DIST>(V, p.tbounds + t * 2 * LP, bwork)) mask |= 1u << uint32_t(t - t0);
-    }
-    if (lane == 0) wmask[wid] = mask;
+  uint32_t consumed = 0;  // ring position (persists across items)
+
+  // Persistent CTA: pull (voxel tile, part) items; parts of a tile are adjacent in the queue so
+  // they run concurrently on different SMs and tighten each other's thresholds via tau_glob.
+  for (;;) {
+    if (tid == 0) *s_item = int(atomicAdd(p.queue, 1u));
     __syncthreads();
-    uint32_t cm = 0;
+    const uint64_t item = uint64_t(uint32_t(*s_item));
+    __syncthreads();
+    if (item >= nitems) break;
+    const uint64_t vt = item / S;
+    const uint32_t part = uint32_t(item % S);
+    const uint64_t nsub = (p.nsuper > part) ? (p.nsuper - part + S - 1) / S : 0;  // super-tiles of this part
+    Voxels<LP, R> V;
+    load_voxels<LP, R>(p, V, tid, vt);
+
+    // ---- seeding: each warp scans first the super-tile of this part nearest its mean TAC ----
+    {
+      int nvalid = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) cm |= wmask[w];
-    const uint32_t mym = wmask[wid];
-    const uint32_t nal = __popc(cm);
-    if (tid == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      uint32_t m = cm;
-      for (uint32_t q = 0; q < nal && q < uint32_t(NST); ++q) {
-        uint32_t b = __ffs(m) - 1;
-        m &= m - 1;
-        issue(t0 + b, int((consumed + q) % NST));
-      }
-    }
-    uint32_t rest = cm;
-    for (uint32_t q = 0; q < nal; ++q) {
-      const uint32_t b = __ffs(rest) - 1;
-      rest &= rest - 1;
-      const uint64_t t = t0 + b;
-      const uint32_t g = consumed + q;
-      const int st = int(g % NST);
-      // every warp observes every phase of the ring (parity waits are only unambiguous when no
-      // phase is skipped), then only the warps whose lanes can improve evaluate the tile
-      mbar_wait(&full[st], (g / NST) & 1u);
-      if ((mym >> b) & 1u) {
-        const float* sb = stage + size_t(st) * Shape<LP>::STAGE_FLOATS;
-        const uint32_t* si = sidx + st * T;
-        const uint64_t rem = N - t * T;
-        const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
-        for (uint32_t d = 0; d < nd; ++d) eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, si[d], work);
+      for (int r = 0; r < R; ++r) nvalid += (V.vox[r] < p.J);
+      nvalid = __reduce_add_sync(0xffffffffu, nvalid);
+      float inv = nvalid > 0 ? 1.0f / float(nvalid) : 0.0f;
+#pragma unroll
+      for (int k = 0; k < LP / 2; ++k) {
+        float2 sm = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (V.vox[r] < p.J) { sm.x += V.y[r][k].x; sm.y += V.y[r][k].y; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          sm.x += __shfl_xor_sync(0xffffffffu, sm.x, o);
+          sm.y += __shfl_xor_sync(0xffffffffu, sm.y, o);
+        }
+        if (lane == 0) {
+          ybar[wid * LP + 2 * k] = sm.x * inv;
+          ybar[wid * LP + 2 * k + 1] = sm.y * inv;
+        }
       }
       __syncwarp();
-      if (lane == 0) {
-        __threadfence_block();
-        int old = atomicAdd(&arrivals[st], 1);
-        if (old == NW - 1) {
-          atomicExch(&arrivals[st], 0);
-          if (q + NST < nal) {
-            uint32_t m = rest;  // tiles after q; the (NST-1)-th of them is q + NST
-            for (int k = 0; k < NST - 1; ++k) m &= m - 1;
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(t0 + (__ffs(m) - 1), st);
+      float best = __int_as_float(0x7f800000);
+      int bi = 0;
+      for (uint64_t k = lane; k < nsub; k += 32) {
+        const float* lo = p.sbounds + (part + k * S) * 2 * LP;
+        const float* hi = lo + LP;
+        float lb = 0.0f;
+        for (int f = 0; f < LP; ++f) {
+          float yk = ybar[wid * LP + f];
+          float g = fmaxf(fmaxf(yk + __ldg(lo + f), -(yk + __ldg(hi + f))), 0.0f);
+          lb = fmaf(g, g, lb);
+          if (lb >= best) break;
+        }
+        if (lb < best) { best = lb; bi = int(k); }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) seeds[wid] = (nvalid > 0 && nsub > 0) ? bi : -1;
+    }
+    __syncthreads();
+    if (tid == 0) {  // drop duplicate seeds (several warps may share their nearest super-tile)
+      for (int w = 1; w < NW; ++w)
+        for (int u = 0; u < w; ++u)
+          if (seeds[w] >= 0 && seeds[u] == seeds[w]) seeds[w] = -1;
+    }
+    __syncthreads();
+
+    for (int64_t it = -NW; it < int64_t(nsub); ++it) {
+      int64_t k;
+      if (it < 0) {
+        k = seeds[it + NW];
+        if (k < 0) continue;
+      } else {
+        k = it;
+        bool is_seed = false;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) is_seed |= (seeds[w] == k);
+        if (is_seed) continue;
+      }
+      if ((it & 7) == 0) refresh_tau<LP, R>(p, V);
+      const uint64_t s = part + uint64_t(k) * S;
+      // super-tile bound
+      bool alive = box_alive<LP, R, DIST>(V, p.sbounds + s * 2 * LP, bwork);
+      if (!__syncthreads_or(alive)) continue;
+      // tile bounds -> per-warp masks
+      const uint64_t t0 = s * kSuper;
+      const uint64_t t1 = (t0 + kSuper < p.ntile) ? t0 + kSuper : p.ntile;
+      uint32_t mask = 0;
+      if (alive) {
+        for (uint64_t t = t0; t < t1; ++t)
+          if (box_alive<LP, R, DIST>(V, p.tbounds + t * 2 * LP, bwork)) mask |= 1u << uint32_t(t - t0);
+      }
+      if (lane == 0) wmask[wid] = mask;
+      __syncthreads();
+      uint32_t cm = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) cm |= wmask[w];
+      const uint32_t mym = wmask[wid];
+      const uint32_t nal = __popc(cm);
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        uint32_t m = cm;
+        for (uint32_t q = 0; q < nal && q < uint32_t(NST); ++q) {
+          uint32_t b = __ffs(m) - 1;
+          m &= m - 1;
+          issue(t0 + b, int((consumed + q) % NST));
+        }
+      }
+      uint32_t rest = cm;
+      for (uint32_t q = 0; q < nal; ++q) {
+        const uint32_t b = __ffs(rest) - 1;
+        rest &= rest - 1;
+        const uint64_t t = t0 + b;
+        const uint32_t g = consumed + q;
+        const int st = int(g % NST);
+        // every warp observes every phase of the ring (parity waits are only unambiguous when no
+        // phase is skipped), then only the warps whose lanes can improve evaluate the tile
+        mbar_wait(&full[st], (g / NST) & 1u);
+        if ((mym >> b) & 1u) {
+          const float* sb = stage + size_t(st) * Shape<LP>::STAGE_FLOATS;
+          const uint32_t* si = sidx + st * T;
+          const uint64_t rem = N - t * T;
+          const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
+          for (uint32_t d = 0; d < nd; ++d) eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, si[d], part, work);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          int old = atomicAdd(&arrivals[st], 1);
+          if (old == NW - 1) {
+            atomicExch(&arrivals[st], 0);
+            if (q + NST < nal) {
+              uint32_t m = rest;  // tiles after q; the (NST-1)-th of them is q + NST
+              for (int kk = 0; kk < NST - 1; ++kk) m &= m - 1;
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              issue(t0 + (__ffs(m) - 1), st);
+            }
           }
         }
       }
+      consumed += nal;
     }
-    consumed += nal;
+    store_counts<LP, R>(p, V, part);
   }
-  finish<LP, R>(p, V, work, bwork, lane, COUNT);
+  finish_counts(p, work, bwork, lane, COUNT);
 }
 
 template <int LP, int DIST, bool COUNT, bool TREE>
@@ -562,8 +605,18 @@ cudaError_t launch_one(const ScanParams& p, cudaStream_t st) {
     attr_set = true;
   }
   uint64_t per_cta = uint64_t(NT) * S::R;
-  unsigned grid = unsigned((p.J + per_cta - 1) / per_cta);
-  kern<<<grid, NT, S::SMEM, st>>>(p);
+  uint64_t nvt = (p.J + per_cta - 1) / per_cta;
+  uint64_t grid = nvt;
+  if (TREE) {  // persistent: one CTA per resident slot, items pulled from p.queue
+    int dev = 0, nsm = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, S::SMEM);
+    uint64_t slots = uint64_t(nsm) * uint64_t(occ > 0 ? occ : 1);
+    uint64_t items = nvt * p.nparts;
+    grid = items < slots ? items : slots;
+  }
+  kern<<<unsigned(grid), NT, S::SMEM, st>>>(p);
   return cudaGetLastError();
 }
 
