@@ -79,6 +79,7 @@ struct abc_ctx {
   // work buffers
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
   DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, tau_glob, queue;
+  DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp;
   abc_stats stats{};
   bool bank_valid = false;
   bool dist_wl2() const { return cfg.distance == ABC_DIST_WL2; }
@@ -494,7 +495,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (tree && eps) nparts = 8u;
   if (nparts > nsuper) nparts = uint32_t(nsuper);
   if (nparts == 0) nparts = 1;
+  const size_t vsort_tmp = tree ? voxel_sort_temp_bytes(J) : 0;
   if (tree) need += N * (8 + 8 + 4 + 4 + 4) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper);
+  if (tree) need += 16 * J + vsort_tmp;
   if (!eps) need += (size_t(8) * K + 4) * J * (nparts - 1) + 4 * J;
   if (!eps) need += size_t(8) * J * K + 4 * J;           // heaps (x nparts in tree mode, below)
   need += size_t(12) * J * (n ? n : 1);                  // exact heaps (fallback)
@@ -525,6 +528,11 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(ctx->sbounds.ensure(sizeof(float) * 2 * LP * nsuper));
     CK(ctx->tau_glob.ensure(4 * J));
     CK(ctx->queue.ensure(16));
+    CK(ctx->vkeys.ensure(4 * J));
+    CK(ctx->vkeys_alt.ensure(4 * J));
+    CK(ctx->vvals.ensure(4 * J));
+    CK(ctx->vorder.ensure(4 * J));
+    CK(ctx->vsort_temp.ensure(vsort_tmp));
   }
   CK(ctx->perm.ensure(sizeof(int) * kMaxLP));
   CK(ctx->wsp.ensure(sizeof(float) * kMaxLP));
@@ -624,6 +632,24 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       op.sbounds = ctx->sbounds.as<float>();
     }
     CK(launch_order(op, st, &launches));
+    if (tree) {
+      VoxelOrderParams vp{};
+      vp.tacs = d_tacs;
+      vp.J = J;
+      vp.L = L;
+      vp.LP = LP;
+      vp.perm = ctx->perm.as<int>();
+      vp.wsp = ctx->wsp.as<float>();
+      vp.mean = ctx->fmean.as<double>();
+      vp.pcs = ctx->pcs.as<float>();
+      vp.keys = ctx->vkeys.as<unsigned int>();
+      vp.keys_alt = ctx->vkeys_alt.as<unsigned int>();
+      vp.vals = ctx->vvals.as<uint32_t>();
+      vp.vorder = ctx->vorder.as<uint32_t>();
+      vp.sort_temp = ctx->vsort_temp.p;
+      vp.sort_temp_bytes = vsort_tmp;
+      CK(launch_voxel_order(vp, st, &launches));
+    }
   }
   rec(EV_ORDER);
 
@@ -660,6 +686,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       sp.nsuper = nsuper;
       sp.tau_glob = eps ? nullptr : ctx->tau_glob.as<unsigned int>();
       sp.queue = ctx->queue.as<unsigned int>();
+      sp.vorder = ctx->vorder.as<uint32_t>();
       if (!eps) launch_fill_u32(ctx->tau_glob.as<uint32_t>(), 0x7f800000u, J, st);
       CK(cudaMemsetAsync(ctx->queue.p, 0, 16, st));
       launches += eps ? 0 : 1;
@@ -813,7 +840,7 @@ void abc_destroy(abc_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs2[] = {&ctx->fmean, &ctx->cov, &ctx->pcs, &ctx->pminmax, &ctx->keys, &ctx->keys_alt, &ctx->vals,
                      &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->tau_glob,
-                     &ctx->queue};
+                     &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,

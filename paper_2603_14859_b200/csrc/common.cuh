@@ -187,6 +187,26 @@ struct OrderParams {
 cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launches);
 size_t order_sort_temp_bytes(uint64_t N);
 
+// Voxel order for the tree scan: voxels sorted by the projection of their prescaled TAC on the
+// bank's first principal axis, so a warp's voxels have similar TACs (smaller alive-tile unions).
+struct VoxelOrderParams {
+  const float* tacs;  // [J][L]
+  uint64_t J;
+  uint32_t L, LP;
+  const int* perm;
+  const float* wsp;
+  const double* mean;  // [L] prescaled frame means (acquisition order)
+  const float* pcs;    // [kNPC][LP]
+  unsigned int* keys;
+  unsigned int* keys_alt;
+  uint32_t* vals;
+  uint32_t* vorder;   // out [J]
+  void* sort_temp;
+  size_t sort_temp_bytes;
+};
+size_t voxel_sort_temp_bytes(uint64_t J);
+cudaError_t launch_voxel_order(const VoxelOrderParams& p, cudaStream_t st, uint32_t* launches);
+
 // Rigorous bound on |D32 - D| for the FP32 pass:
 //   err(D) = a D + b sqrt(Y2 D) + c Y2 + d Y1,  Y2 = sum_f w_f y_f^2, Y1 = sum_f w_f |y_f|.
 struct ErrBound {
@@ -229,6 +249,7 @@ struct ScanParams {
   uint32_t nparts;
   unsigned int* tau_glob;   // [J] float bits (positive), atomicMin
   unsigned int* queue;      // work-queue counter (zeroed per run)
+  const uint32_t* vorder;   // [J] voxel processed in slot j (tree mode) or nullptr (identity)
 };
 constexpr int MOMW = 2 + 2 * ABC_MAX_P + 2;  // count, (S1,S2) x P, (KS1, KS2), pad
 cudaError_t launch_scan(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);

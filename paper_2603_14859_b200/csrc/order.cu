@@ -293,7 +293,48 @@ __global__ void __launch_bounds__(128) super_bounds_kernel(const OrderParams p, 
   }
 }
 
+__global__ void __launch_bounds__(256) voxel_key_kernel(const VoxelOrderParams p) {
+  __shared__ float sm_mu[kMaxLP], sm_wsp[kMaxLP], sm_pc[kMaxLP];
+  __shared__ int sm_perm[kMaxLP];
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    int src = p.perm[k];
+    sm_perm[k] = src;
+    sm_wsp[k] = p.wsp[k];
+    sm_mu[k] = src >= 0 ? float(p.mean[src]) : 0.0f;
+    sm_pc[k] = p.pcs[k];
+  }
+  __syncthreads();
+  for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < p.J; j += uint64_t(gridDim.x) * blockDim.x) {
+    const float* y = p.tacs + j * p.L;
+    float pr = 0.0f;
+    for (uint32_t k = 0; k < p.LP; ++k) {
+      int src = sm_perm[k];
+      if (src < 0) break;
+      pr = fmaf(sm_wsp[k] * __ldg(y + src) - sm_mu[k], sm_pc[k], pr);
+    }
+    p.keys[j] = f2ord(pr);
+    p.vals[j] = uint32_t(j);
+  }
+}
+
 }  // namespace
+
+size_t voxel_sort_temp_bytes(uint64_t J) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned int*)nullptr, (unsigned int*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, int(J), 0, 32);
+  return bytes;
+}
+
+cudaError_t launch_voxel_order(const VoxelOrderParams& p, cudaStream_t st, uint32_t* launches) {
+  voxel_key_kernel<<<148 * 4, 256, 0, st>>>(p);
+  size_t tb = p.sort_temp_bytes;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(p.sort_temp, tb, p.keys, p.keys_alt, p.vals, p.vorder, int(p.J), 0,
+                                                  32, st);
+  *launches += 5;
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
 
 size_t order_sort_temp_bytes(uint64_t N) {
   size_t bytes = 0;

@@ -30,7 +30,7 @@
 namespace vpet {
 namespace scan {
 
-constexpr int NT = 256;
+constexpr int NT = 128;
 constexpr int NW = NT / 32;
 constexpr int NST = 4;
 constexpr int CH = 8;
@@ -39,7 +39,7 @@ constexpr int T = kTile;
 template <int LP>
 struct Shape {
   static constexpr int R = (LP <= 48) ? 2 : 1;
-  static constexpr int MINB = (LP * R <= 96) ? 2 : 1;
+  static constexpr int MINB = (LP * R <= 96) ? 4 : 2;
   static constexpr size_t STAGE_FLOATS = size_t(T) * LP;
   static constexpr size_t SMEM = size_t(NST) * (STAGE_FLOATS * 4 + T * 4) + NST * 8 + NST * 4 +
                                  NW * 4 + NW * 4 + NW * LP * 4 + 16 + 64;
@@ -159,9 +159,10 @@ __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& 
   const float INF = __int_as_float(0x7f800000);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    uint64_t v = vtile * (NT * R) + uint64_t(r) * NT + tid;
+    uint64_t slot = vtile * (NT * R) + uint64_t(r) * NT + tid;
+    bool valid = slot < p.J;
+    uint64_t v = (valid && p.vorder) ? uint64_t(__ldg(p.vorder + slot)) : slot;
     V.vox[r] = v;
-    bool valid = v < p.J;
     const float* yr = p.tacs + (valid ? v : 0) * p.L;
 #pragma unroll
     for (int k = 0; k < LP; k += 2) {
