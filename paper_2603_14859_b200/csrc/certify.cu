@@ -258,7 +258,11 @@ __global__ void certify_reduce_kernel(const ReduceParams p, uint32_t Kp, uint32_
       cnt = nc;
     }
     __syncwarp();
-    warp_sort_pairs(cd, ci, Kp, lane);
+    {
+      uint32_t kp = 32;  // sort only the occupied power of two
+      while (kp < cnt) kp <<= 1;
+      warp_sort_pairs(cd, ci, kp < Kp ? kp : Kp, lane);
+    }
     if (!p.exact && tK < __int_as_float(0x7f800000)) {
       double Y2 = 0.0, Y1 = 0.0;
       for (uint32_t f = lane; f < p.L; f += 32) {

@@ -93,9 +93,11 @@ struct Phi {
 
 __device__ inline Phi phi_all(double x) {
   Phi r;
-  if (x < 0.5) {
-    // coefficients: p1: 1/(k+1)!, ps: 1/(k+2)!, ch: (k+1)/(k+2)!, om: (k+2)/(k+3)!, alternating.
-    double p1 = 0.0, ps = 0.0, ch = 0.0, om = 0.0;
+  if (x == 0.0) {
+    r.e = 1.0; r.p1 = 1.0; r.ps = 0.5; r.ch = 0.5; r.om = 1.0 / 3.0;
+  } else if (x < 0.5) {
+    // coefficients: p1: 1/(k+1)!, ps: 1/(k+2)!, om: (k+2)/(k+3)!, alternating in x.
+    double p1 = 0.0, ps = 0.0, om = 0.0;
     double f1 = 1.0 / 6402373705728000.0;  // 1/18!
     double f2 = f1 / 19.0, f3 = f2 / 20.0;  // 1/19!, 1/20!
 #pragma unroll
@@ -103,14 +105,15 @@ __device__ inline Phi phi_all(double x) {
       // f1 = 1/(k+1)!, f2 = 1/(k+2)!, f3 = 1/(k+3)!
       p1 = fma(p1, -x, f1);
       ps = fma(ps, -x, f2);
-      ch = fma(ch, -x, double(k + 1) * f2);
       om = fma(om, -x, double(k + 2) * f3);
       f3 = f2; f2 = f1; f1 = f1 * double(k + 1);
     }
-    r.p1 = p1; r.ps = ps; r.ch = ch; r.om = om;
-    r.e = exp(-x);
+    r.p1 = p1; r.ps = ps; r.om = om;
+    r.ch = p1 - ps;           // ~1/2: no cancellation
+    r.e = fma(-x, p1, 1.0);   // 1 - x p1 = e^-x; x p1 <= 0.4
   } else {
-    double e = exp(-x), em1 = -expm1(-x);  // 1 - e^-x
+    double e = exp(-x);
+    double em1 = 1.0 - e;     // e <= 0.61: no cancellation
     double ix = 1.0 / x;
     r.e = e;
     r.p1 = em1 * ix;

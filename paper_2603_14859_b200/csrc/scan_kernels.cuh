@@ -147,11 +147,10 @@ static __device__ __noinline__ void eps_candidate(const float* yrow, const float
 template <int LP, int R>
 struct Voxels {
   float2 y[R][LP / 2];
-  float tau[R];   // insertion threshold: min(own heap root, shared tau_glob) (top-n) / eps bound
-  float tp[R];    // pruning threshold (tau, or +inf with ABC_FLAG_NO_PRUNE)
+  float tau[R];   // threshold: min(own heap root, shared tau_glob) (top-n) / eps bound; prunes too
   float taup[R];  // own (part) heap root, +inf until the heap is full
   uint32_t cnt[R];
-  uint64_t vox[R];
+  uint32_t vox[R];  // voxel index (>= J for an empty slot)
 };
 
 template <int LP, int R>
@@ -162,7 +161,7 @@ __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& 
     uint64_t slot = vtile * (NT * R) + uint64_t(r) * NT + tid;
     bool valid = slot < p.J;
     uint64_t v = (valid && p.vorder) ? uint64_t(__ldg(p.vorder + slot)) : slot;
-    V.vox[r] = v;
+    V.vox[r] = uint32_t(v);
     const float* yr = p.tacs + (valid ? v : 0) * p.L;
 #pragma unroll
     for (int k = 0; k < LP; k += 2) {
@@ -189,7 +188,6 @@ __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& 
       // candidates: D32 <= eps + err(eps)  <=>  D32 < next float above it
       V.tau[r] = valid ? nextafterf(__double2float_ru(p.eps + err), INF) : -INF;
     }
-    V.tp[r] = (p.prune || !valid) ? V.tau[r] : INF;
   }
 }
 
@@ -249,10 +247,10 @@ __device__ __forceinline__ void bound_chunk(const Voxels<LP, R>& V, const float*
 }
 
 template <int LP, int R>
-__device__ __forceinline__ bool any_alive(const Voxels<LP, R>& V, const float2 (&acc)[R]) {
-  bool alive = false;
+__device__ __forceinline__ bool any_alive(const Voxels<LP, R>& V, const float2 (&acc)[R], bool noprune) {
+  bool alive = noprune;
 #pragma unroll
-  for (int r = 0; r < R; ++r) alive |= (__fadd_rn(acc[r].x, acc[r].y) < V.tp[r]);
+  for (int r = 0; r < R; ++r) alive |= (__fadd_rn(acc[r].x, acc[r].y) < V.tau[r]);
   return __any_sync(0xffffffffu, alive);
 }
 
@@ -261,12 +259,12 @@ template <int LP, int R, int DIST, bool BOUND, int C>
 struct Chunks {
   static constexpr int NCH = (LP + CH - 1) / CH;
   __device__ __forceinline__ static bool run(const Voxels<LP, R>& V, const float* a, const float* b, float2 (&acc)[R],
-                                             unsigned long long& work) {
+                                             unsigned long long& work, bool noprune) {
     if (BOUND) bound_chunk<LP, R, DIST, C>(V, a, b, acc);
     else dist_chunk<LP, R, DIST, C>(V, a, acc);
     work += uint64_t(((C + 1) * CH < LP ? (C + 1) * CH : LP) - C * CH) * R;
-    if (!any_alive<LP, R>(V, acc)) return false;
-    if constexpr (C + 1 < NCH) return Chunks<LP, R, DIST, BOUND, C + 1>::run(V, a, b, acc, work);
+    if (!any_alive<LP, R>(V, acc, noprune)) return false;
+    if constexpr (C + 1 < NCH) return Chunks<LP, R, DIST, BOUND, C + 1>::run(V, a, b, acc, work, noprune);
     return true;
   }
 };
@@ -279,7 +277,7 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
   unsigned long long w = 0;
-  bool go = Chunks<LP, R, DIST, false, 0>::run(V, sr, nullptr, acc, w);
+  bool go = Chunks<LP, R, DIST, false, 0>::run(V, sr, nullptr, acc, w, !p.prune);
   if (COUNT) work += w;
   if (go) {
 #pragma unroll
@@ -288,15 +286,14 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
       if (D < V.tau[r]) {
         if (!p.eps_mode) {
           unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
-          uint2 st = heap_push(p.heap + (V.vox[r] * p.nparts + part) * p.K, p.K, V.cnt[r], key);
+          uint2 st = heap_push(p.heap + (uint64_t(V.vox[r]) * p.nparts + part) * p.K, p.K, V.cnt[r], key);
           V.cnt[r] = st.x;
           V.taup[r] = __uint_as_float(st.y);
           if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + V.vox[r], st.y);
           V.tau[r] = fminf(V.tau[r], V.taup[r]);
-          if (p.prune) V.tp[r] = V.tau[r];
         } else {
-          eps_candidate(p.tacs + V.vox[r] * p.L, p.bank, p.LS, p.w, p.L, p.dist, p.eps,
-                        p.mom + V.vox[r] * (size_t(p.M) * MOMW), p.prior_g, i);
+          eps_candidate(p.tacs + uint64_t(V.vox[r]) * p.L, p.bank, p.LS, p.w, p.L, p.dist, p.eps,
+                        p.mom + uint64_t(V.vox[r]) * (size_t(p.M) * MOMW), p.prior_g, i);
         }
       }
     }
@@ -312,7 +309,6 @@ __device__ __forceinline__ void refresh_tau(const ScanParams& p, Voxels<LP, R>& 
     if (V.vox[r] < p.J) {
       float g = __uint_as_float(__ldcg(p.tau_glob + V.vox[r]));
       V.tau[r] = fminf(V.tau[r], g);
-      if (p.prune) V.tp[r] = V.tau[r];
     }
   }
 }
@@ -322,14 +318,14 @@ __device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const float* b
   float2 acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
-  return Chunks<LP, R, DIST, true, 0>::run(V, box, box + LP, acc, work);
+  return Chunks<LP, R, DIST, true, 0>::run(V, box, box + LP, acc, work, false);
 }
 
 template <int LP, int R>
 __device__ __forceinline__ void store_counts(const ScanParams& p, const Voxels<LP, R>& V, uint32_t part) {
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if (V.vox[r] < p.J && !p.eps_mode) p.heap_cnt[V.vox[r] * p.nparts + part] = V.cnt[r];
+    if (V.vox[r] < p.J && !p.eps_mode) p.heap_cnt[uint64_t(V.vox[r]) * p.nparts + part] = V.cnt[r];
 }
 
 __device__ __forceinline__ void finish_counts(const ScanParams& p, unsigned long long work, unsigned long long bwork,

@@ -85,7 +85,8 @@ def launches(path, dst):
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0][:100]
-        scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(r[ui], 1.0)
+        scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3,
+                 "s": 1e3}.get(r[ui], 1.0)
         tot[name] += float(r[vi].replace(",", "")) * scale
         cnt[name] += 1
     T = sum(tot.values())
