@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvpetabc.so")
+LIB_PATH = os.environ.get("VPET_LIB") or os.path.join(_HERE, "libvpetabc.so")  # VPET_LIB: tuning builds only
 
 MAX_P = 8
 MAX_MODELS = 4

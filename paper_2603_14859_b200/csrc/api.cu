@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -491,8 +492,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
   // draw-range split of the tree scan (interleaved super-tiles): balances heavy voxels over SMs
   uint32_t nparts = 1;
-  if (tree && !eps) nparts = K <= 64 ? 8u : (K <= 512 ? 2u : 1u);
-  if (tree && eps) nparts = 8u;
+  if (tree && !eps) nparts = K <= 64 ? 4u : (K <= 512 ? 2u : 1u);
+  if (tree && eps) nparts = 4u;
+  if (const char* e = getenv("VPET_NPARTS")) nparts = uint32_t(std::max(1, atoi(e)));  // tuning knob
   if (nparts > nsuper) nparts = uint32_t(nsuper);
   if (nparts == 0) nparts = 1;
   const size_t vsort_tmp = tree ? voxel_sort_temp_bytes(J) : 0;

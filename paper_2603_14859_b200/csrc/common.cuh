@@ -11,8 +11,14 @@ namespace vpet {
 constexpr uint32_t kCtrTag = 0x56504554u;  // "VPET": 4th Philox counter word (R7)
 constexpr int kMaxLP = 128;
 constexpr int kNPC = 4;      // principal axes used for the draw order (order.cu)
-constexpr int kTile = 64;    // draws per tile (bounding box + TMA transfer unit)
-constexpr int kSuper = 16;   // tiles per super-tile
+#ifndef VPET_TILE
+#define VPET_TILE 64
+#endif
+#ifndef VPET_SUPER
+#define VPET_SUPER 16
+#endif
+constexpr int kTile = VPET_TILE;    // draws per tile (bounding box + TMA transfer unit)
+constexpr int kSuper = VPET_SUPER;  // tiles per super-tile (<= 32: one bit per tile in a mask)
 constexpr int kMaxGrid = 8192;  // max points of a draw-independent time grid
 
 // ---------------------------------------------------------------------------------------

@@ -33,7 +33,10 @@ namespace scan {
 constexpr int NT = 128;
 constexpr int NW = NT / 32;
 constexpr int NST = 4;
-constexpr int CH = 8;
+#ifndef VPET_CH
+#define VPET_CH 8
+#endif
+constexpr int CH = VPET_CH;  // frames per pruning chunk (multiple of 4)
 constexpr int T = kTile;
 
 template <int LP>

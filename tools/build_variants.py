@@ -1,0 +1,23 @@
+"""Build tuning variants of libvpetabc.so into tune/ (compile-time VPET_TILE / VPET_SUPER / VPET_CH)."""
+import concurrent.futures as cf
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2603_14859_b200 import build as B  # noqa: E402
+
+VARIANTS = {
+    "base": (),
+    "ch4": ("VPET_CH=4",),
+    "t32s32": ("VPET_TILE=32", "VPET_SUPER=32"),
+    "t64s8": ("VPET_SUPER=8",),
+    "t32s16": ("VPET_TILE=32", "VPET_SUPER=16"),
+}
+names = sys.argv[1:] or list(VARIANTS)
+root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
+os.makedirs(root, exist_ok=True)
+with cf.ThreadPoolExecutor(max_workers=2) as ex:
+    futs = {n: ex.submit(B.build, True, False, os.path.join(root, f"libvpetabc_{n}.so"), VARIANTS[n] or ("VPET_BASE=1",))
+            for n in names}
+    for n, f in futs.items():
+        print(n, f.result(), flush=True)
