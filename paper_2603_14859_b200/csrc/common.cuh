@@ -12,10 +12,10 @@ constexpr uint32_t kCtrTag = 0x56504554u;  // "VPET": 4th Philox counter word (D
 constexpr int kMaxLP = 128;
 constexpr int kNPC = 4;      // principal axes used for the draw order (order.cu)
 #ifndef VPET_TILE
-#define VPET_TILE 64
+#define VPET_TILE 32
 #endif
 #ifndef VPET_SUPER
-#define VPET_SUPER 16
+#define VPET_SUPER 32
 #endif
 constexpr int kTile = VPET_TILE;    // draws per tile (bounding box + TMA transfer unit)
 constexpr int kSuper = VPET_SUPER;  // tiles per super-tile (<= 32: one bit per tile in a mask)

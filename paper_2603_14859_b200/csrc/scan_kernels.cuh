@@ -30,22 +30,32 @@
 namespace vpet {
 namespace scan {
 
-constexpr int NT = 128;
+#ifndef VPET_NT
+#define VPET_NT 64
+#endif
+#ifndef VPET_NST
+#define VPET_NST 3
+#endif
+constexpr int NT = VPET_NT;   // threads per CTA (the warps of a CTA share tile loads)
 constexpr int NW = NT / 32;
-constexpr int NST = 4;
+constexpr int NST = VPET_NST;  // TMA ring stages
 #ifndef VPET_CH
-#define VPET_CH 8
+#define VPET_CH 12
 #endif
 constexpr int CH = VPET_CH;  // frames per pruning chunk (multiple of 4)
 constexpr int T = kTile;
+#ifndef VPET_SEEDS
+#define VPET_SEEDS 2
+#endif
+constexpr int MS = VPET_SEEDS;  // nearest super-tiles each warp scans first (seeding)
 
 template <int LP>
 struct Shape {
   static constexpr int R = (LP <= 48) ? 2 : 1;
-  static constexpr int MINB = (LP * R <= 96) ? 4 : 2;
+  static constexpr int MINB = ((LP * R <= 96) ? 16 : 8) / NW;
   static constexpr size_t STAGE_FLOATS = size_t(T) * LP;
   static constexpr size_t SMEM = size_t(NST) * (STAGE_FLOATS * 4 + T * 4) + NST * 8 + NST * 4 +
-                                 NW * 4 + NW * 4 + NW * LP * 4 + 16 + 64;
+                                 NW * 4 + NW * MS * 4 + NW * LP * 4 + 16 + 64;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
@@ -418,7 +428,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
   int* arrivals = reinterpret_cast<int*>(full + NST);
   uint32_t* wmask = reinterpret_cast<uint32_t*>(arrivals + NST);
   int* seeds = reinterpret_cast<int*>(wmask + NW);
-  float* ybar = reinterpret_cast<float*>(seeds + NW);
+  float* ybar = reinterpret_cast<float*>(seeds + NW * MS);
   int* s_item = reinterpret_cast<int*>(ybar + NW * LP);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -484,46 +494,56 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
         }
       }
       __syncwarp();
-      float best = __int_as_float(0x7f800000);
-      int bi = 0;
-      for (uint64_t k = lane; k < nsub; k += 32) {
-        const float* lo = p.sbounds + (part + k * S) * 2 * LP;
-        const float* hi = lo + LP;
-        float lb = 0.0f;
-        for (int f = 0; f < LP; ++f) {
-          float yk = ybar[wid * LP + f];
-          float g = fmaxf(fmaxf(yk + __ldg(lo + f), -(yk + __ldg(hi + f))), 0.0f);
-          lb = fmaf(g, g, lb);
-          if (lb >= best) break;
-        }
-        if (lb < best) { best = lb; bi = int(k); }
-      }
+      int chosen[MS];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        float ob = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob < best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      for (int m = 0; m < MS; ++m) {
+        float best = __int_as_float(0x7f800000);
+        int bi = -1;
+        for (uint64_t k = lane; k < nsub; k += 32) {
+          bool taken = false;
+#pragma unroll
+          for (int u = 0; u < MS; ++u) taken |= (u < m && chosen[u] == int(k));
+          if (taken) continue;
+          const float* lo = p.sbounds + (part + k * S) * 2 * LP;
+          const float* hi = lo + LP;
+          float lb = 0.0f;
+          for (int f = 0; f < LP; ++f) {
+            float yk = ybar[wid * LP + f];
+            float g = fmaxf(fmaxf(yk + __ldg(lo + f), -(yk + __ldg(hi + f))), 0.0f);
+            lb = fmaf(g, g, lb);
+            if (lb >= best) break;
+          }
+          if (lb < best) { best = lb; bi = int(k); }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          float ob = __shfl_xor_sync(0xffffffffu, best, o);
+          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (oi >= 0 && (bi < 0 || ob < best || (ob == best && oi < bi))) { best = ob; bi = oi; }
+        }
+        chosen[m] = bi;
+        if (lane == 0) seeds[wid * MS + m] = (nvalid > 0) ? bi : -1;
       }
-      if (lane == 0) seeds[wid] = (nvalid > 0 && nsub > 0) ? bi : -1;
     }
     __syncthreads();
-    if (tid == 0) {  // drop duplicate seeds (several warps may share their nearest super-tile)
-      for (int w = 1; w < NW; ++w)
-        for (int u = 0; u < w; ++u)
-          if (seeds[w] >= 0 && seeds[u] == seeds[w]) seeds[w] = -1;
+    if (tid == 0) {  // drop duplicate seeds (warps may share their nearest super-tiles)
+      for (int a = 1; a < NW * MS; ++a)
+        for (int b = 0; b < a; ++b)
+          if (seeds[a] >= 0 && seeds[b] == seeds[a]) seeds[a] = -1;
     }
     __syncthreads();
 
-    for (int64_t it = -NW; it < int64_t(nsub); ++it) {
+    for (int64_t it = -NW * MS; it < int64_t(nsub); ++it) {
       int64_t k;
-      if (it < 0) {
-        k = seeds[it + NW];
+      if (it < 0) {  // seeds by rank: every warp's nearest first, then the second nearest, ...
+        const int q = int(it + NW * MS);
+        k = seeds[(q % NW) * MS + q / NW];
         if (k < 0) continue;
       } else {
         k = it;
         bool is_seed = false;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) is_seed |= (seeds[w] == k);
+        for (int w = 0; w < NW * MS; ++w) is_seed |= (seeds[w] == k);
         if (is_seed) continue;
       }
       if ((it & 7) == 0) refresh_tau<LP, R>(p, V);

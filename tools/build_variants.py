@@ -7,11 +7,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
-    "base": (),
-    "ch4": ("VPET_CH=4",),
-    "t32s32": ("VPET_TILE=32", "VPET_SUPER=32"),
-    "t64s8": ("VPET_SUPER=8",),
-    "t32s16": ("VPET_TILE=32", "VPET_SUPER=16"),
+    "ch12": ("VPET_CH=12",),
+    "ch16": ("VPET_CH=16",),
+    "ch20": ("VPET_CH=20",),
+    "ch36": ("VPET_CH=36",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
