@@ -7,10 +7,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
-    "ch12": ("VPET_CH=12",),
+    "base": (),
     "ch16": ("VPET_CH=16",),
-    "ch20": ("VPET_CH=20",),
-    "ch36": ("VPET_CH=36",),
+    "nt128": ("VPET_NT=128",),
+    "seeds1": ("VPET_SEEDS=1",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
