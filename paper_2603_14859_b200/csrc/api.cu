@@ -499,7 +499,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (nparts == 0) nparts = 1;
   const size_t vsort_tmp = tree ? voxel_sort_temp_bytes(J) : 0;
   if (tree) need += N * (8 + 8 + 4 + 4 + 4) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper);
-  if (tree) need += 16 * J + vsort_tmp;
+  if (tree) need += 24 * J + vsort_tmp;
   if (!eps) need += (size_t(8) * K + 4) * J * (nparts - 1) + 4 * J;
   if (!eps) need += size_t(8) * J * K + 4 * J;           // heaps (x nparts in tree mode, below)
   need += size_t(12) * J * (n ? n : 1);                  // exact heaps (fallback)
@@ -530,8 +530,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(ctx->sbounds.ensure(sizeof(float) * 2 * LP * nsuper));
     CK(ctx->tau_glob.ensure(4 * J));
     CK(ctx->queue.ensure(16));
-    CK(ctx->vkeys.ensure(4 * J));
-    CK(ctx->vkeys_alt.ensure(4 * J));
+    CK(ctx->vkeys.ensure(8 * J));
+    CK(ctx->vkeys_alt.ensure(8 * J));
     CK(ctx->vvals.ensure(4 * J));
     CK(ctx->vorder.ensure(4 * J));
     CK(ctx->vsort_temp.ensure(vsort_tmp));
@@ -644,8 +644,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       vp.wsp = ctx->wsp.as<float>();
       vp.mean = ctx->fmean.as<double>();
       vp.pcs = ctx->pcs.as<float>();
-      vp.keys = ctx->vkeys.as<unsigned int>();
-      vp.keys_alt = ctx->vkeys_alt.as<unsigned int>();
+      vp.pminmax = ctx->pminmax.as<unsigned int>();
+      vp.keys = ctx->vkeys.as<unsigned long long>();
+      vp.keys_alt = ctx->vkeys_alt.as<unsigned long long>();
       vp.vals = ctx->vvals.as<uint32_t>();
       vp.vorder = ctx->vorder.as<uint32_t>();
       vp.sort_temp = ctx->vsort_temp.p;

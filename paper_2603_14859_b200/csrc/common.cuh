@@ -206,8 +206,9 @@ struct VoxelOrderParams {
   const float* wsp;
   const double* mean;  // [L] prescaled frame means (acquisition order)
   const float* pcs;    // [kNPC][LP]
-  unsigned int* keys;
-  unsigned int* keys_alt;
+  const unsigned int* pminmax;  // [2 kNPC] bank projection range (order-preserving uint of float)
+  unsigned long long* keys;
+  unsigned long long* keys_alt;
   uint32_t* vals;
   uint32_t* vorder;   // out [J]
   void* sort_temp;

@@ -293,26 +293,71 @@ __global__ void __launch_bounds__(128) super_bounds_kernel(const OrderParams p, 
   }
 }
 
+// Voxel scan order.  VPET_VOXKEY = 1: first-principal-axis projection; D = 2 or 4: D-dimensional
+// Morton code of the projection on the first D principal axes, on the bank's isotropic grid.
+#ifndef VPET_VOXKEY
+#define VPET_VOXKEY 2
+#endif
+#ifndef VPET_VOXS
+#define VPET_VOXS 0.5f
+#endif
+constexpr int kVoxDims = VPET_VOXKEY;
+constexpr int kVoxAxisBits = kVoxDims == 1 ? 32 : (kVoxDims == 2 ? 16 : (kVoxDims == 3 ? 20 : 15));
+constexpr int kVoxBits = kVoxDims * kVoxAxisBits;
+
+__device__ __forceinline__ unsigned long long spread_d(unsigned long long x) {
+  unsigned long long r = 0;
+#pragma unroll
+  for (int b = 0; b < kVoxAxisBits; ++b) r |= ((x >> b) & 1ull) << (kVoxDims * b);
+  return r;
+}
+
 __global__ void __launch_bounds__(256) voxel_key_kernel(const VoxelOrderParams p) {
-  __shared__ float sm_mu[kMaxLP], sm_wsp[kMaxLP], sm_pc[kMaxLP];
+  __shared__ float sm_mu[kMaxLP], sm_wsp[kMaxLP], sm_pc[kNPC * kMaxLP];
   __shared__ int sm_perm[kMaxLP];
+  __shared__ float sm_lo[kNPC], sm_scale;
   for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
     int src = p.perm[k];
     sm_perm[k] = src;
     sm_wsp[k] = p.wsp[k];
     sm_mu[k] = src >= 0 ? float(p.mean[src]) : 0.0f;
-    sm_pc[k] = p.pcs[k];
+  }
+  for (uint32_t e = threadIdx.x; e < kNPC * p.LP; e += blockDim.x) sm_pc[e] = p.pcs[e];
+  if (threadIdx.x == 0) {
+    float rng = 0.0f;
+    for (int c = 0; c < kNPC; ++c) {
+      sm_lo[c] = ord2f(p.pminmax[2 * c]);
+      rng = fmaxf(rng, ord2f(p.pminmax[2 * c + 1]) - sm_lo[c]);
+    }
+    const float top = float((1u << (kVoxDims == 1 ? 15 : kVoxAxisBits)) - 1u);
+    sm_scale = rng > 0.0f ? top / rng : 0.0f;
   }
   __syncthreads();
   for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < p.J; j += uint64_t(gridDim.x) * blockDim.x) {
     const float* y = p.tacs + j * p.L;
-    float pr = 0.0f;
+    float pr[kVoxDims];
+#pragma unroll
+    for (int c = 0; c < kVoxDims; ++c) pr[c] = 0.0f;
     for (uint32_t k = 0; k < p.LP; ++k) {
       int src = sm_perm[k];
       if (src < 0) break;
-      pr = fmaf(sm_wsp[k] * __ldg(y + src) - sm_mu[k], sm_pc[k], pr);
+      const float x = sm_wsp[k] * __ldg(y + src) - sm_mu[k];
+#pragma unroll
+      for (int c = 0; c < kVoxDims; ++c) pr[c] = fmaf(x, sm_pc[c * p.LP + k], pr[c]);
     }
-    p.keys[j] = f2ord(pr);
+    unsigned long long key = 0;
+    if (kVoxDims == 1) {
+      key = f2ord(pr[0]);
+    } else {
+      const float top = float((1u << kVoxAxisBits) - 1u);
+#pragma unroll
+      for (int c = 0; c < kVoxDims; ++c) {
+        const float sc = c == 0 ? sm_scale : sm_scale * VPET_VOXS;
+        const float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sc, 0.0f), top);
+        key |= spread_d((unsigned long long)q) << (kVoxDims - 1 - c);
+      }
+    }
+    p.keys[j] = key;
     p.vals[j] = uint32_t(j);
   }
 }
@@ -321,8 +366,8 @@ __global__ void __launch_bounds__(256) voxel_key_kernel(const VoxelOrderParams p
 
 size_t voxel_sort_temp_bytes(uint64_t J) {
   size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned int*)nullptr, (unsigned int*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, int(J), 0, 32);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, int(J), 0, kVoxBits);
   return bytes;
 }
 
@@ -330,7 +375,7 @@ cudaError_t launch_voxel_order(const VoxelOrderParams& p, cudaStream_t st, uint3
   voxel_key_kernel<<<148 * 4, 256, 0, st>>>(p);
   size_t tb = p.sort_temp_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(p.sort_temp, tb, p.keys, p.keys_alt, p.vals, p.vorder, int(p.J), 0,
-                                                  32, st);
+                                                  kVoxBits, st);
   *launches += 5;
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

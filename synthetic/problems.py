@@ -355,3 +355,100 @@ def config4_chunk(chunk=0, n_chunks=32, N=10_000_000, n=18, seed=1004, abc_seed=
               seed=abc_seed, distance=distance, accept="TOPN", n_accept=n)
     return Problem(f"config4_chunk{chunk}of{n_chunks}", kw, "PWL", kv, kt, start, dur,
                    decay_weights(start, dur, T_HALF_F18), y, dict(theta=theta, label=lab, z=zz, clean=C))
+
+
+# ----------------------------------------------------------------------------------
+# config 3: brain phantom 128 x 128 x 63, whole volume, MRTM vs lp-ntPET, 90 x 60 s
+# ----------------------------------------------------------------------------------
+BRAIN_SHAPE = (63, 128, 128)  # (z, y, x)
+# class: (R1, k2, BP) means; k2a = k2 / (1 + BP) (MRTM kinetics, eq:lp-ntPET with gamma = 0)
+BRAIN_CLASSES = {
+    0: ("outside", (0.05, 0.05, 0.0)),
+    1: ("white", (0.70, 0.20, 0.5)),
+    2: ("grey", (1.00, 0.30, 1.0)),
+    3: ("cerebellum", (1.00, 0.18, 0.0)),
+    4: ("striatum", (1.00, 0.35, 3.0)),
+    5: ("striatum_active", (1.00, 0.35, 3.0)),
+}
+
+
+def brain_geometry(z):
+    """Class label of every voxel of axial slice z (raster order, 128 x 128)."""
+    nz, ny, nx = BRAIN_SHAPE
+    cz, cy, cx = (nz - 1) / 2.0, (ny - 1) / 2.0, (nx - 1) / 2.0
+    yy, xx = np.mgrid[0:ny, 0:nx].astype(np.float64)
+
+    def ell(x0, y0, z0, ax, ay, az):
+        return ((xx - x0) / ax) ** 2 + ((yy - y0) / ay) ** 2 + ((z - z0) / az) ** 2 <= 1.0
+
+    lab = np.zeros((ny, nx), dtype=np.int32)
+    rb = np.sqrt(((xx - cx) / 50.0) ** 2 + ((yy - cy) / 57.0) ** 2 + ((z - cz - 4) / 27.0) ** 2)
+    brain = rb <= 1.0
+    lab[brain] = 1
+    lab[brain & (rb > 0.85)] = 2
+    lab[ell(cx, cy + 38, 10, 30, 16, 9)] = 3  # cerebellum: posterior, inferior
+    for side in (-1, 1):  # caudate (x0 +-12) and putamen (x0 +-24) ellipsoids
+        lab[ell(cx + side * 12, cy - 14, cz + 6, 5, 9, 7)] = 4
+        lab[ell(cx + side * 24, cy - 4, cz + 2, 6, 12, 8)] = 4
+    # activated sub-region: dorsal half of the left putamen and left caudate head
+    act = (ell(cx - 24, cy - 4, cz + 2, 6, 12, 8) & (yy < cy - 4)) | (ell(cx - 12, cy - 14, cz + 6, 5, 9, 7) & (yy < cy - 16))
+    lab[act] = 5
+    return lab.ravel()
+
+
+def config3(slices=None, N=10_000_000, n=100, noise="mid", seed=1003, abc_seed=2026, device="cpu",
+            max_voxels=None, voxel_index=None, distance="WL2", lpnt_step_min=0.05):
+    """Brain phantom: every voxel of the 128 x 128 x 63 volume (or of
+    `slices`), striatal ellipsoids with an activated sub-region (gamma > 0, onset and peak per
+    the config-2 recipe, region-wide with voxel jitter), cerebellar reference region,
+    reference TAC = 1TCM(0.1, 0.3) (x) Feng, 90 x 60 s frames, Gaussian noise of
+    P:229 at the config-2 level `noise`; N = 1e7 draws split between MRTM and lp-ntPET, n = 100."""
+    start, dur = uniform_frames(90, 60.0)
+    zs = range(BRAIN_SHAPE[0]) if slices is None else slices
+    labs, zz = [], []
+    for z in zs:
+        lab = brain_geometry(z)
+        labs.append(lab)
+        zz.append(np.full(lab.shape, z, dtype=np.int32))
+    lab = np.concatenate(labs)
+    zz = np.concatenate(zz)
+    flat = np.concatenate([np.arange(BRAIN_SHAPE[1] * BRAIN_SHAPE[2]) for _ in zs])
+    if voxel_index is not None:
+        lab, zz, flat = lab[voxel_index], zz[voxel_index], flat[voxel_index]
+    if max_voxels is not None:
+        lab, zz, flat = lab[:max_voxels], zz[:max_voxels], flat[:max_voxels]
+    J = len(lab)
+    rng = np.random.default_rng([seed, 0])
+    region = np.random.default_rng([seed, 1])  # region-wide activation timing
+    tD0 = region.uniform(30.0, 40.0)
+    tP0 = region.uniform(tD0 + 2.0, 45.0)
+    al0 = float(np.clip(region.normal(0.7, 0.1), 0.3, None))
+    base = np.array([BRAIN_CLASSES[c][1] for c in range(len(BRAIN_CLASSES))], dtype=np.float64)[lab]
+    jit = np.exp(0.1 * rng.standard_normal((J, 3)))
+    R1 = base[:, 0] * jit[:, 0]
+    k2 = base[:, 1] * jit[:, 1]
+    bp = base[:, 2] * jit[:, 2]
+    k2a = k2 / (1.0 + bp)
+    active = lab == 5
+    gam = np.where(active, 0.35 * k2a * np.exp(0.1 * rng.standard_normal(J)), 0.0)
+    tD = tD0 + 0.5 * rng.standard_normal(J)
+    tP = np.maximum(tP0 + 0.5 * rng.standard_normal(J), tD + 1.0)
+    al = np.clip(al0 + 0.02 * rng.standard_normal(J), 0.3, None)
+    theta = np.stack([R1, k2, k2a, gam, tD, tP, al], axis=1)
+    cr, C = truth_rt(theta, FENG_PHANTOM, (0.1, 0.3), start, dur, device)
+    lam = math.log(2.0) / T_HALF_C11
+    mid = start + 0.5 * dur
+    late = slice(-10, None)
+    ref_mask = lab == 3
+    cref = float(np.mean(C[ref_mask][:, late])) if ref_mask.any() else float(np.mean(cr[late]))
+    ell1 = NOISE_CV[noise] * math.sqrt(cref * 1.0 * math.exp(lam * float(np.mean(mid[late]))))
+    y = noise_rt_gauss(C, start, dur, ell1, T_HALF_C11, rng).astype(np.float32)
+    lo, hi = priors_rt()
+    half = N // 2
+    kw = dict(models=[dict(kind="MRTM", n_draws=half, lo=lo, hi=hi),
+                      dict(kind="LPNTPET", n_draws=N - half, lo=lo, hi=hi)],
+              seed=abc_seed, distance=distance, accept="TOPN", n_accept=n, lpnt_step_min=lpnt_step_min)
+    kt = np.concatenate([[0.0], mid])
+    kv = np.concatenate([[0.0], cr])
+    return Problem("config3", kw, "PWL", kv, kt, start, dur, decay_weights(start, dur, T_HALF_C11), y,
+                   dict(theta=theta, active=active, label=lab, z=zz, flat=flat, clean=C, ref=cr, ell1=ell1))

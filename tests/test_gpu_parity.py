@@ -26,6 +26,15 @@ def rt_small():
     return S.config2(J=96, N_per_model=4000, n=40, noise="mid")
 
 
+@pytest.fixture(scope="module")
+def brain_small():
+    # config-3-shaped: brain phantom voxels of every class (incl. the activated striatum), 90 frames
+    lab = np.concatenate([S.brain_geometry(z) for z in (10, 33, 35)])
+    rng = np.random.default_rng(7)
+    idx = np.sort(np.concatenate([rng.choice(np.flatnonzero(lab == c), 16, replace=False) for c in range(6)]))
+    return S.config3(slices=(10, 33, 35), voxel_index=idx, N=8000, n=40)
+
+
 def test_bank_matches_oracle_rn32(cfg1, tb_small, rt_small):
     """Alg.1 l.3: the GPU bank equals the oracle's RN32 frame averages (rare 1-ulp flips of
     values within FP64 rounding of an FP32 tie are allowed)."""
@@ -72,6 +81,14 @@ def test_rt_model_selection(rt_small):
     g, _ = run_gpu(rt_small)
     o, _ = run_oracle(rt_small)
     compare(g, o)
+
+
+def test_brain_model_selection(brain_small):
+    """Config-3 shape: L = 90 (the widest frame count of the configs), MRTM vs lp-ntPET."""
+    g, _ = run_gpu(brain_small)
+    o, _ = run_oracle(brain_small)
+    rep = compare(g, o)
+    assert rep["matched"] >= brain_small.J - 2
 
 
 @pytest.mark.parametrize("flags", [0x2, 0x8, 0x10, 0x8 | 0x10, 0x20, 0x20 | 0x8])

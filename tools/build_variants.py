@@ -8,9 +8,7 @@ from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": (),
-    "ch16": ("VPET_CH=16",),
-    "nt128": ("VPET_NT=128",),
-    "seeds1": ("VPET_SEEDS=1",),
+    "pc1": ("VPET_VOXKEY=1",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
