@@ -35,7 +35,7 @@ PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "scan_ncu_summary.json")
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--draws", type=int, default=10_000_000)
@@ -68,6 +68,9 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thr = threading.Thread(target=self._read, daemon=True)
             self.thr.start()
+            t0 = time.time()  # let nvidia-smi initialise before the timed region starts
+            while not self.rows and time.time() - t0 < 5.0:
+                time.sleep(0.05)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -296,7 +299,7 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "draws/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "step_ms": [round(v, 3) for v in step_ms], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "config4: total-body 50-min FDG phantom 192x192x673 (4.44M voxels), 2TCM "
                                    "k4=0 vs k4>0 (M=2), N=1e7 draws, n=18, L=35, weighted L2; one step = axial "
