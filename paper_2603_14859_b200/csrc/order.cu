@@ -198,6 +198,14 @@ __global__ void __launch_bounds__(256) proj_minmax_kernel(const OrderParams p) {
   }
 }
 
+// bank Morton grid: scale of principal axes 2..4 relative to the isotropic grid, and whether the
+// first axis takes the most significant bit of each 4-bit group
+#ifndef VPET_BANKS
+#define VPET_BANKS 1.0f
+#endif
+#ifndef VPET_BANK_MSB
+#define VPET_BANK_MSB 0
+#endif
 __device__ __forceinline__ unsigned long long spread4(unsigned long long x) {
   // insert 3 zero bits between the low 15 bits of x (4-D Morton)
   unsigned long long r = 0;
@@ -231,8 +239,9 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
     unsigned long long key = 0;
 #pragma unroll
     for (int c = 0; c < kNPC; ++c) {
-      float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sm_scale, 0.0f), 32767.0f);
-      key |= spread4((unsigned long long)q) << c;
+      const float sc = c == 0 ? sm_scale : sm_scale * VPET_BANKS;
+      float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sc, 0.0f), 32767.0f);
+      key |= spread4((unsigned long long)q) << (VPET_BANK_MSB ? kNPC - 1 - c : c);
     }
     p.keys[i] = key;
     p.vals[i] = uint32_t(i);

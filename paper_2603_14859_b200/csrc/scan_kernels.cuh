@@ -52,7 +52,11 @@ constexpr int MS = VPET_SEEDS;  // nearest super-tiles each warp scans first (se
 template <int LP>
 struct Shape {
   static constexpr int R = (LP <= 48) ? 2 : 1;
+#ifdef VPET_MINB
+  static constexpr int MINB = VPET_MINB;
+#else
   static constexpr int MINB = ((LP * R <= 96) ? 16 : 8) / NW;
+#endif
   static constexpr size_t STAGE_FLOATS = size_t(T) * LP;
   static constexpr size_t SMEM = size_t(NST) * (STAGE_FLOATS * 4 + T * 4) + NST * 8 + NST * 4 +
                                  NW * 4 + NW * MS * 4 + NW * LP * 4 + 16 + 64;
@@ -291,7 +295,10 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
   for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
   unsigned long long w = 0;
   bool go = Chunks<LP, R, DIST, false, 0>::run(V, sr, nullptr, acc, w, !p.prune);
-  if (COUNT) work += w;
+#ifndef VPET_COUNT_PUSH
+#define VPET_COUNT_PUSH 0  // tuning: count heap pushes instead of frame updates
+#endif
+  if (COUNT && !VPET_COUNT_PUSH) work += w;
   if (go) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -299,6 +306,7 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
       if (D < V.tau[r]) {
         if (!p.eps_mode) {
           unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
+          if (COUNT && VPET_COUNT_PUSH) work += 1;
           uint2 st = heap_push(p.heap + (uint64_t(V.vox[r]) * p.nparts + part) * p.K, p.K, V.cnt[r], key);
           V.cnt[r] = st.x;
           V.taup[r] = __uint_as_float(st.y);
