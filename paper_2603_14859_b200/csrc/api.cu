@@ -80,7 +80,7 @@ struct abc_ctx {
   DevBuf d_fdur, d_fs, d_fe, d_favg, d_w, d_wsc, d_gt, d_gc, d_gframe, d_ft, d_fc, d_fframe;
   // work buffers
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
-  DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, tau_glob, queue;
+  DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, hbounds, tau_glob, queue;
   DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp;
   abc_stats stats{};
   bool bank_valid = false;
@@ -504,10 +504,19 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (tree && !eps) nparts = K <= 64 ? 4u : (K <= 512 ? 2u : 1u);
   if (tree && eps) nparts = 4u;
   if (const char* e = getenv("VPET_NPARTS")) nparts = uint32_t(std::max(1, atoi(e)));  // tuning knob
-  if (nparts > nsuper) nparts = uint32_t(nsuper);
+  // hyper-tiles of hs super-tiles: the unit of the work split and of the best-first order; at most
+  // kHyperSort per part
+  uint32_t hs = 16;
+  if (const char* e = getenv("VPET_HS")) hs = uint32_t(std::max(1, atoi(e)));  // tuning knob
+  {
+    const uint64_t need_hs = (nsuper + uint64_t(kHyperSort) * nparts - 1) / (uint64_t(kHyperSort) * nparts);
+    if (need_hs > hs) hs = uint32_t(need_hs);
+  }
+  const uint64_t nhyper = (nsuper + hs - 1) / hs;
+  if (nparts > nhyper) nparts = uint32_t(nhyper);
   if (nparts == 0) nparts = 1;
   const size_t vsort_tmp = tree ? voxel_sort_temp_bytes(J) : 0;
-  if (tree) need += N * (8 + 8 + 4 + 4 + 4) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper);
+  if (tree) need += N * (8 + 8 + 4 + 4 + 4) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper + nhyper);
   if (tree) need += 24 * J + vsort_tmp;
   if (!eps) need += (size_t(8) * K + 4) * J * (nparts - 1) + 4 * J;
   if (!eps) need += size_t(8) * J * K + 4 * J;           // heaps (x nparts in tree mode, below)
@@ -541,6 +550,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(ctx->sort_temp.ensure(sort_tmp));
     CK(ctx->tbounds.ensure(sizeof(float) * 2 * LP * ntile));
     CK(ctx->sbounds.ensure(sizeof(float) * 2 * LP * nsuper));
+    CK(ctx->hbounds.ensure(sizeof(float) * 2 * LP * nhyper));
     CK(ctx->tau_glob.ensure(4 * J));
     CK(ctx->queue.ensure(16));
     CK(ctx->vkeys.ensure(8 * J));
@@ -647,6 +657,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       op.sort_temp_bytes = sort_tmp;
       op.tbounds = ctx->tbounds.as<float>();
       op.sbounds = ctx->sbounds.as<float>();
+      op.hbounds = ctx->hbounds.as<float>();
+      op.hs = hs;
+      op.nhyper = nhyper;
     }
     CK(launch_order(op, st, &launches));
     if (tree) {
@@ -700,6 +713,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       sp.idxmap = ctx->idxmap.as<uint32_t>();
       sp.tbounds = ctx->tbounds.as<float>();
       sp.sbounds = ctx->sbounds.as<float>();
+      sp.hbounds = ctx->hbounds.as<float>();
+      sp.nhyper = nhyper;
+      sp.hs = hs;
       sp.ntile = ntile;
       sp.nsuper = nsuper;
       sp.tau_glob = eps ? nullptr : ctx->tau_glob.as<unsigned int>();
@@ -860,7 +876,7 @@ void abc_destroy(abc_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs2[] = {&ctx->fmean, &ctx->cov, &ctx->pcs, &ctx->pminmax, &ctx->keys, &ctx->keys_alt, &ctx->vals,
-                     &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->tau_glob,
+                     &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob,
                      &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,

@@ -20,6 +20,7 @@ namespace {
 __device__ __forceinline__ double exact_distance_c(const float* y, const float* s, const float* w, uint32_t L,
                                                    int dist) {
   double D = 0.0;
+#pragma unroll 8
   for (uint32_t f = 0; f < L; ++f) {
     double d = __dsub_rn(double(__ldg(y + f)), double(__ldg(s + f)));
     double t = (dist == ABC_DIST_L1) ? fabs(d) : __dmul_rn(d, d);

@@ -192,6 +192,9 @@ struct OrderParams {
   size_t sort_temp_bytes;
   float* tbounds;     // [ntile][2][LP] per-tile min/max of bankp
   float* sbounds;     // [nsuper][2][LP]
+  float* hbounds;     // [nhyper][2][LP] (hyper-tile = hs consecutive super-tiles)
+  uint32_t hs;
+  uint64_t nhyper;
 };
 cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launches);
 size_t order_sort_temp_bytes(uint64_t N);
@@ -252,15 +255,18 @@ struct ScanParams {
   const uint32_t* idxmap;   // [N] draw index of scan row j
   const float* tbounds;     // [ntile][2][LP]
   const float* sbounds;     // [nsuper][2][LP]
-  uint64_t ntile, nsuper;
+  const float* hbounds;     // [nhyper][2][LP]
+  uint64_t ntile, nsuper, nhyper;
+  uint32_t hs;              // super-tiles per hyper-tile
   unsigned long long* bound_work;  // LB frame-evaluation counter (COUNT)
-  // work split: item = (voxel tile, part); part p owns super-tiles s = p (mod nparts) and its own
+  // work split: item = (voxel tile, part); part p owns hyper-tiles h = p (mod nparts) and its own
   // heap [J][nparts][K]; tau_glob[v] = min over parts of their heap thresholds (shared pruning)
   uint32_t nparts;
   unsigned int* tau_glob;   // [J] float bits (positive), atomicMin
   unsigned int* queue;      // work-queue counter (zeroed per run)
   const uint32_t* vorder;   // [J] voxel processed in slot j (tree mode) or nullptr (identity)
 };
+constexpr int kHyperSort = 256;  // max hyper-tiles per part (best-first order sorted in shared memory)
 constexpr int MOMW = 2 + 2 * ABC_MAX_P + 2;  // count, (S1,S2) x P, (KS1, KS2), pad
 cudaError_t launch_scan(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);
 cudaError_t launch_scan_wl2(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);

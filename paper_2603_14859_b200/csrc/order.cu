@@ -65,6 +65,11 @@ __global__ void frame_perm_kernel(const OrderParams p) {
     p.perm[k] = src;
     p.wsp[k] = src >= 0 ? p.wsc[src] : 0.0f;
   }
+  if (p.tree && p.pminmax)  // projection range accumulators (order-preserving uint of float)
+    for (int c = 0; c < kNPC; ++c) {
+      p.pminmax[2 * c] = 0xffffffffu;
+      p.pminmax[2 * c + 1] = 0u;
+    }
 }
 
 // ---- covariance of the prescaled bank (scan order), one block per (row, col) pair ----
@@ -97,50 +102,59 @@ __global__ void __launch_bounds__(256) cov_kernel(const OrderParams p) {
 }
 
 // ---- top-NPC eigenvectors by power iteration with deflation (one block) ----
-__global__ void __launch_bounds__(128) pca_kernel(const OrderParams p) {
-  __shared__ double C[kMaxLP * kMaxLP / 4];  // LP <= 128 handled in chunks below
+// ---- first kNPC principal axes of the covariance: power iteration with deflation, one warp;
+// stops when the direction changes by < 1e-9 (eigen-gaps of a bank are large) or after 100 steps ----
+__global__ void __launch_bounds__(32) pca_kernel(const OrderParams p) {
+  __shared__ double C[kMaxLP * kMaxLP / 4];  // LP <= 64; larger LP works from global memory
   __shared__ double v[kMaxLP], w[kMaxLP];
-  __shared__ double nrm;
   const uint32_t LP = p.LP;
-  // C may not fit for LP = 128 (128 KB); work from global memory in that case.
+  const int lane = threadIdx.x;
   const bool in_smem = LP * LP <= kMaxLP * kMaxLP / 4;
   double* Cm = in_smem ? C : p.cov;
   if (in_smem)
-    for (uint32_t e = threadIdx.x; e < LP * LP; e += blockDim.x) C[e] = p.cov[e];
-  __syncthreads();
+    for (uint32_t e = lane; e < LP * LP; e += 32) C[e] = p.cov[e];
+  __syncwarp();
+  auto wsum = [](double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+  };
   for (int c = 0; c < kNPC; ++c) {
-    for (uint32_t k = threadIdx.x; k < LP; k += blockDim.x) v[k] = 1.0 + 0.001 * double((k * 7919u + c * 104729u) % 97u);
-    __syncthreads();
-    for (int it = 0; it < 60; ++it) {  // eigen-gaps of the bank are large; 60 steps converge
-      for (uint32_t k = threadIdx.x; k < LP; k += blockDim.x) {
+    for (uint32_t k = lane; k < LP; k += 32) v[k] = 1.0 + 0.001 * double((k * 7919u + c * 104729u) % 97u);
+    __syncwarp();
+    for (int it = 0; it < 100; ++it) {
+      double ss = 0.0;
+      for (uint32_t k = lane; k < LP; k += 32) {
         double s = 0.0;
         for (uint32_t g = 0; g < LP; ++g) s += Cm[k * LP + g] * v[g];
         w[k] = s;
+        ss += s * s;
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (uint32_t k = 0; k < LP; ++k) s += w[k] * w[k];
-        nrm = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+      ss = wsum(ss);
+      const double nrm = ss > 0.0 ? 1.0 / sqrt(ss) : 0.0;
+      double dd = 0.0;
+      __syncwarp();
+      for (uint32_t k = lane; k < LP; k += 32) {
+        const double nv = w[k] * nrm;
+        dd += (nv - v[k]) * (nv - v[k]);
+        v[k] = nv;
       }
-      __syncthreads();
-      for (uint32_t k = threadIdx.x; k < LP; k += blockDim.x) v[k] = w[k] * nrm;
-      __syncthreads();
+      dd = wsum(dd);
+      __syncwarp();
+      if (dd < 1e-18) break;
     }
     // eigenvalue and deflation
-    if (threadIdx.x == 0) {
-      double lam = 0.0;
-      for (uint32_t k = 0; k < LP; ++k) {
-        double s = 0.0;
-        for (uint32_t g = 0; g < LP; ++g) s += Cm[k * LP + g] * v[g];
-        lam += v[k] * s;
-      }
-      nrm = lam;
+    double lam = 0.0;
+    for (uint32_t k = lane; k < LP; k += 32) {
+      double s = 0.0;
+      for (uint32_t g = 0; g < LP; ++g) s += Cm[k * LP + g] * v[g];
+      lam += v[k] * s;
     }
-    __syncthreads();
-    for (uint32_t e = threadIdx.x; e < LP * LP; e += blockDim.x) Cm[e] -= nrm * v[e / LP] * v[e % LP];
-    for (uint32_t k = threadIdx.x; k < LP; k += blockDim.x) p.pcs[c * LP + k] = float(v[k]);
-    __syncthreads();
+    lam = wsum(lam);
+    __syncwarp();
+    for (uint32_t e = lane; e < LP * LP; e += 32) Cm[e] -= lam * v[e / LP] * v[e % LP];
+    for (uint32_t k = lane; k < LP; k += 32) p.pcs[c * LP + k] = float(v[k]);
+    __syncwarp();
   }
 }
 
@@ -203,6 +217,10 @@ __global__ void __launch_bounds__(256) proj_minmax_kernel(const OrderParams p) {
 #ifndef VPET_BANKS
 #define VPET_BANKS 1.0f
 #endif
+#ifndef VPET_MBITS
+#define VPET_MBITS 15  // Morton bits per principal axis of the bank order
+#endif
+constexpr int kMBits = VPET_MBITS;
 #ifndef VPET_BANK_MSB
 #define VPET_BANK_MSB 0
 #endif
@@ -230,7 +248,7 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
       sm_lo[c] = ord2f(p.pminmax[2 * c]);
       rng = fmaxf(rng, ord2f(p.pminmax[2 * c + 1]) - sm_lo[c]);
     }
-    sm_scale = rng > 0.0f ? 32767.0f / rng : 0.0f;  // isotropic grid, 15 bits on the widest axis
+    sm_scale = rng > 0.0f ? float((1u << kMBits) - 1u) / rng : 0.0f;  // isotropic grid, kMBits on the widest axis
   }
   __syncthreads();
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.N; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -240,7 +258,7 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
 #pragma unroll
     for (int c = 0; c < kNPC; ++c) {
       const float sc = c == 0 ? sm_scale : sm_scale * VPET_BANKS;
-      float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sc, 0.0f), 32767.0f);
+      float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sc, 0.0f), float((1u << kMBits) - 1u));
       key |= spread4((unsigned long long)q) << (VPET_BANK_MSB ? kNPC - 1 - c : c);
     }
     p.keys[i] = key;
@@ -299,6 +317,21 @@ __global__ void __launch_bounds__(128) super_bounds_kernel(const OrderParams p, 
     }
     p.sbounds[(s * 2 + 0) * p.LP + k] = lo;
     p.sbounds[(s * 2 + 1) * p.LP + k] = hi;
+  }
+}
+
+__global__ void __launch_bounds__(128) hyper_bounds_kernel(const OrderParams p, uint64_t nsup) {
+  uint64_t h = blockIdx.x;
+  uint64_t s0 = h * p.hs;
+  uint64_t s1 = s0 + p.hs < nsup ? s0 + p.hs : nsup;
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    float lo = 3.0e38f, hi = -3.0e38f;
+    for (uint64_t s = s0; s < s1; ++s) {
+      lo = fminf(lo, p.sbounds[(s * 2 + 0) * p.LP + k]);
+      hi = fmaxf(hi, p.sbounds[(s * 2 + 1) * p.LP + k]);
+    }
+    p.hbounds[(h * 2 + 0) * p.LP + k] = lo;
+    p.hbounds[(h * 2 + 1) * p.LP + k] = hi;
   }
 }
 
@@ -393,7 +426,7 @@ cudaError_t launch_voxel_order(const VoxelOrderParams& p, cudaStream_t st, uint3
 size_t order_sort_temp_bytes(uint64_t N) {
   size_t bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, int(N), 0, kNPC * 15);
+                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, int(N), 0, kNPC * kMBits);
   return bytes;
 }
 
@@ -405,19 +438,13 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
   if (p.tree) {
     cudaMemsetAsync(p.cov, 0, sizeof(double) * p.LP * p.LP, st);
     cov_kernel<<<dim3(p.LP, p.LP), 256, 0, st>>>(p);
-    pca_kernel<<<1, 128, 0, st>>>(p);
-    unsigned int init[2 * kNPC];
-    for (int c = 0; c < kNPC; ++c) {
-      init[2 * c] = 0xffffffffu;
-      init[2 * c + 1] = 0u;
-    }
-    cudaMemcpyAsync(p.pminmax, init, sizeof init, cudaMemcpyHostToDevice, st);
+    pca_kernel<<<1, 32, 0, st>>>(p);
     proj_minmax_kernel<<<148 * 4, 256, 0, st>>>(p);
     key_kernel<<<148 * 8, 256, 0, st>>>(p);
     *launches += 4;
     size_t tb = p.sort_temp_bytes;
     cudaError_t e = cub::DeviceRadixSort::SortPairs(p.sort_temp, tb, p.keys, p.keys_alt, p.vals, p.order, int(p.N), 0,
-                                                    kNPC * 15, st);
+                                                    kNPC * kMBits, st);
     if (e != cudaSuccess) return e;
     *launches += 4;  // onesweep: histogram + passes (approximate count of CUB launches)
   } else {
@@ -430,7 +457,8 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
     uint64_t nsup = (ntile + kSuper - 1) / kSuper;
     tile_bounds_kernel<<<unsigned(ntile), 128, 0, st>>>(p);
     super_bounds_kernel<<<unsigned(nsup), 128, 0, st>>>(p, ntile);
-    *launches += 2;
+    hyper_bounds_kernel<<<unsigned(p.nhyper), 128, 0, st>>>(p, nsup);
+    *launches += 3;
   }
   return cudaGetLastError();
 }

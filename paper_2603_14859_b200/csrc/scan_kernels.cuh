@@ -44,10 +44,9 @@ constexpr int NST = VPET_NST;  // TMA ring stages
 #endif
 constexpr int CH = VPET_CH;  // frames per pruning chunk (multiple of 4)
 constexpr int T = kTile;
-#ifndef VPET_SEEDS
-#define VPET_SEEDS 2
+#ifndef VPET_SSORT
+#define VPET_SSORT 1
 #endif
-constexpr int MS = VPET_SEEDS;  // nearest super-tiles each warp scans first (seeding)
 
 template <int LP>
 struct Shape {
@@ -59,7 +58,7 @@ struct Shape {
 #endif
   static constexpr size_t STAGE_FLOATS = size_t(T) * LP;
   static constexpr size_t SMEM = size_t(NST) * (STAGE_FLOATS * 4 + T * 4) + NST * 8 + NST * 4 +
-                                 NW * 4 + NW * MS * 4 + NW * LP * 4 + 16 + 64;
+                                 NW * 4 + NW * LP * 4 + 16 + 64 + size_t(kHyperSort) * (NW * 8 + 8 + NW * 4) + kHyperSort / 8;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
@@ -423,8 +422,90 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_flat_kernel(const Sc
   finish_counts(p, work, 0ull, lane, COUNT);
 }
 
+// Ascending bitonic sort of P2 (a power of two) keys in shared memory by the whole CTA.
+__device__ __forceinline__ void cta_bitonic(unsigned long long* key, uint32_t P2, int tid) {
+  for (uint32_t kk = 2; kk <= P2; kk <<= 1) {
+    for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (uint32_t i = tid; i < P2; i += NT) {
+        const uint32_t l = i ^ jj;
+        if (l > i) {
+          const unsigned long long a = key[i], b = key[l];
+          if ((a > b) == ((i & kk) == 0)) { key[i] = b; key[l] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Best-first visiting order of n boxes for the CTA: each warp ranks the boxes by the lower bound of
+// its mean TAC (lbs[w][k]); the CTA order alternates between the warps' rankings (warp 0's best,
+// warp 1's best, warp 0's second, ...) skipping boxes already taken and warps without voxels.
+// keys: [NW * kHyperSort] scratch; order: [kHyperSort] output; vis: [kHyperSort / 32] scratch.
+__device__ __forceinline__ void best_first(const float* lbs, uint32_t n, unsigned long long* keys, uint32_t* order,
+                                           uint32_t* vis, int tid) {
+  uint32_t P2 = 1;
+  while (P2 < n) P2 <<= 1;
+  for (uint32_t e = tid; e < NW * P2; e += NT) {
+    const uint32_t w = e / P2, k = e % P2;
+    const uint32_t lbb = k < n ? __float_as_uint(lbs[w * kHyperSort + k]) : 0x7fffffffu;
+    keys[e] = (static_cast<unsigned long long>(w) << 62) | (static_cast<unsigned long long>(lbb) << 16) | k;
+  }
+  for (uint32_t e = tid; e < kHyperSort / 32; e += NT) vis[e] = 0u;
+  __syncthreads();
+  cta_bitonic(keys, NW * P2, tid);
+  if (tid == 0) {
+    uint32_t ptr[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) ptr[w] = 0;
+    uint32_t q = 0, turn = 0;
+    while (q < n) {
+      bool took = false;
+      for (int a = 0; a < NW && !took; ++a) {
+        const uint32_t w = (turn + a) % NW;
+        while (ptr[w] < n) {
+          const unsigned long long kk = keys[w * P2 + ptr[w]];
+          const uint32_t k = uint32_t(kk & 0xffffu), lbb = uint32_t((kk >> 16) & 0x7fffffffu);
+          if (lbb >= 0x7f800000u) { ptr[w] = n; break; }  // warp without voxels (or no bound)
+          if ((vis[k >> 5] >> (k & 31)) & 1u) { ++ptr[w]; continue; }
+          vis[k >> 5] |= 1u << (k & 31);
+          order[q++] = k;
+          ++ptr[w];
+          took = true;
+          break;
+        }
+      }
+      if (!took) {  // every ranking exhausted: append the rest in index order
+        for (uint32_t k = 0; k < n; ++k)
+          if (!((vis[k >> 5] >> (k & 31)) & 1u)) order[q++] = k;
+        break;
+      }
+      turn = (turn + 1) % NW;
+    }
+  }
+  __syncthreads();
+}
+
+// Lower bound of a mean TAC (shared memory, LP frames) against a box [lo; hi] (global memory).
+template <int LP>
+__device__ __forceinline__ float mean_lb(const float* yb, const float* lo) {
+  const float* hi = lo + LP;
+  float lb = 0.0f;
+  for (int f = 0; f < LP; f += 4) {
+    const float4 l4 = __ldg(reinterpret_cast<const float4*>(lo + f));
+    const float4 h4 = __ldg(reinterpret_cast<const float4*>(hi + f));
+    const float l[4] = {l4.x, l4.y, l4.z, l4.w}, h[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float g = fmaxf(fmaxf(yb[f + u] + l[u], -(yb[f + u] + h[u])), 0.0f);
+      lb = fmaf(g, g, lb);
+    }
+  }
+  return lb;
+}
+
 // =============================================================================================
-// Tree scan: Morton-ordered bank, super-tile / tile bounds, seeding.
+// Tree scan: Morton-ordered bank, hyper-tile / super-tile / tile bounds, best-first order.
 // =============================================================================================
 template <int LP, int DIST, bool COUNT>
 __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const ScanParams p) {
@@ -435,9 +516,14 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NST * (Shape<LP>::STAGE_FLOATS * 4 + T * 4));
   int* arrivals = reinterpret_cast<int*>(full + NST);
   uint32_t* wmask = reinterpret_cast<uint32_t*>(arrivals + NST);
-  int* seeds = reinterpret_cast<int*>(wmask + NW);
-  float* ybar = reinterpret_cast<float*>(seeds + NW * MS);
+  float* ybar = reinterpret_cast<float*>(wmask + NW);
   int* s_item = reinterpret_cast<int*>(ybar + NW * LP);
+  unsigned long long* okeys = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(s_item + 4) + 15) & ~uintptr_t(15));  // [NW][kHyperSort] sort scratch
+  uint32_t* horder = reinterpret_cast<uint32_t*>(okeys + NW * kHyperSort);  // [kHyperSort] hyper-tile order
+  uint32_t* sorder = horder + kHyperSort;                                  // [kHyperSort] super-tile order
+  uint32_t* vis = sorder + kHyperSort;                                     // [kHyperSort / 32]
+  float* hlb = reinterpret_cast<float*>(vis + kHyperSort / 32);            // [NW][kHyperSort]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t N = p.N;
@@ -474,16 +560,20 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
     if (item >= nitems) break;
     const uint64_t vt = item / S;
     const uint32_t part = uint32_t(item % S);
-    const uint64_t nsub = (p.nsuper > part) ? (p.nsuper - part + S - 1) / S : 0;  // super-tiles of this part
+    const uint64_t nsub = (p.nhyper > part) ? (p.nhyper - part + S - 1) / S : 0;  // hyper-tiles of this part
     Voxels<LP, R> V;
     load_voxels<LP, R>(p, V, tid, vt);
 
-    // ---- seeding: each warp scans first the super-tile of this part nearest its mean TAC ----
+    // ---- best-first order of this part's hyper-tiles: key = min over warps of the lower bound of
+    // the warp's mean TAC against the hyper-tile box (a heuristic order; exactness does not depend
+    // on it).  Sorted in shared memory (bitonic), then scanned in that order.
+    bool wvalid;
     {
       int nvalid = 0;
 #pragma unroll
       for (int r = 0; r < R; ++r) nvalid += (V.vox[r] < p.J);
       nvalid = __reduce_add_sync(0xffffffffu, nvalid);
+      wvalid = nvalid > 0;
       float inv = nvalid > 0 ? 1.0f / float(nvalid) : 0.0f;
 #pragma unroll
       for (int k = 0; k < LP / 2; ++k) {
@@ -502,62 +592,35 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
         }
       }
       __syncwarp();
-      int chosen[MS];
-#pragma unroll
-      for (int m = 0; m < MS; ++m) {
-        float best = __int_as_float(0x7f800000);
-        int bi = -1;
-        for (uint64_t k = lane; k < nsub; k += 32) {
-          bool taken = false;
-#pragma unroll
-          for (int u = 0; u < MS; ++u) taken |= (u < m && chosen[u] == int(k));
-          if (taken) continue;
-          const float* lo = p.sbounds + (part + k * S) * 2 * LP;
-          const float* hi = lo + LP;
-          float lb = 0.0f;
-          for (int f = 0; f < LP; ++f) {
-            float yk = ybar[wid * LP + f];
-            float g = fmaxf(fmaxf(yk + __ldg(lo + f), -(yk + __ldg(hi + f))), 0.0f);
-            lb = fmaf(g, g, lb);
-            if (lb >= best) break;
-          }
-          if (lb < best) { best = lb; bi = int(k); }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          float ob = __shfl_xor_sync(0xffffffffu, best, o);
-          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (oi >= 0 && (bi < 0 || ob < best || (ob == best && oi < bi))) { best = ob; bi = oi; }
-        }
-        chosen[m] = bi;
-        if (lane == 0) seeds[wid * MS + m] = (nvalid > 0) ? bi : -1;
+      for (uint64_t k = lane; k < nsub; k += 32) {
+        const float lb = mean_lb<LP>(ybar + wid * LP, p.hbounds + (part + k * S) * 2 * LP);
+        hlb[wid * kHyperSort + k] = wvalid ? lb : __int_as_float(0x7f800000);
       }
     }
     __syncthreads();
-    if (tid == 0) {  // drop duplicate seeds (warps may share their nearest super-tiles)
-      for (int a = 1; a < NW * MS; ++a)
-        for (int b = 0; b < a; ++b)
-          if (seeds[a] >= 0 && seeds[b] == seeds[a]) seeds[a] = -1;
-    }
-    __syncthreads();
+    best_first(hlb, uint32_t(nsub), okeys, horder, vis, tid);
 
-    for (int64_t it = -NW * MS; it < int64_t(nsub); ++it) {
-      int64_t k;
-      if (it < 0) {  // seeds by rank: every warp's nearest first, then the second nearest, ...
-        const int q = int(it + NW * MS);
-        k = seeds[(q % NW) * MS + q / NW];
-        if (k < 0) continue;
-      } else {
-        k = it;
-        bool is_seed = false;
-#pragma unroll
-        for (int w = 0; w < NW * MS; ++w) is_seed |= (seeds[w] == k);
-        if (is_seed) continue;
+    uint32_t it = 0;
+    for (uint32_t q = 0; q < nsub; ++q) {
+      const uint64_t h = part + uint64_t(horder[q]) * S;
+      if ((q & 3) == 0) refresh_tau<LP, R>(p, V);
+      const bool halive = box_alive<LP, R, DIST>(V, p.hbounds + h * 2 * LP, bwork);
+      if (!__syncthreads_or(halive)) continue;
+      const uint64_t s0 = h * p.hs;
+      const uint32_t ns = uint32_t(((s0 + p.hs < p.nsuper) ? s0 + p.hs : p.nsuper) - s0);
+      const bool ssort = VPET_SSORT && ns <= uint32_t(kHyperSort);
+      if (ssort) {  // best-first order of the super-tiles inside the hyper-tile
+        for (uint32_t k = lane; k < ns; k += 32)
+          hlb[wid * kHyperSort + k] =
+              wvalid ? mean_lb<LP>(ybar + wid * LP, p.sbounds + (s0 + k) * 2 * LP) : __int_as_float(0x7f800000);
+        __syncthreads();
+        best_first(hlb, ns, okeys, sorder, vis, tid);
       }
-      if ((it & 7) == 0) refresh_tau<LP, R>(p, V);
-      const uint64_t s = part + uint64_t(k) * S;
+      for (uint32_t u = 0; u < ns; ++u, ++it) {
+      const uint64_t s = s0 + (ssort ? sorder[u] : u);
+      if ((it & 7) == 7) refresh_tau<LP, R>(p, V);
       // super-tile bound
-      bool alive = box_alive<LP, R, DIST>(V, p.sbounds + s * 2 * LP, bwork);
+      bool alive = halive && box_alive<LP, R, DIST>(V, p.sbounds + s * 2 * LP, bwork);
       if (!__syncthreads_or(alive)) continue;
       // tile bounds -> per-warp masks
       const uint64_t t0 = s * kSuper;
@@ -616,6 +679,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
         }
       }
       consumed += nal;
+      }
     }
     store_counts<LP, R>(p, V, part);
   }
