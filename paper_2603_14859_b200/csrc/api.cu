@@ -518,8 +518,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const size_t vsort_tmp = tree ? voxel_sort_temp_bytes(J) : 0;
   if (tree) need += N * (8 + 8 + 4 + 4 + 4) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper + nhyper);
   if (tree) need += 24 * J + vsort_tmp;
-  if (!eps) need += (size_t(8) * K + 4) * J * (nparts - 1) + 4 * J;
-  if (!eps) need += size_t(8) * J * K + 4 * J;           // heaps (x nparts in tree mode, below)
+  if (!eps) need += (size_t(8) * heap_stride(std::max<uint32_t>(K, 1)) + 4) * J * nparts + 4 * J;  // heaps
   need += size_t(12) * J * (n ? n : 1);                  // exact heaps (fallback)
   if (eps) need += sizeof(double) * J * M * MOMW;
   if (host_tacs) need += sizeof(float) * J * L;
@@ -562,7 +561,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   CK(ctx->perm.ensure(sizeof(int) * kMaxLP));
   CK(ctx->wsp.ensure(sizeof(float) * kMaxLP));
   if (!eps) {
-    CK(ctx->heap.ensure(size_t(8) * J * nparts * std::max<uint32_t>(K, 1)));
+    CK(ctx->heap.ensure(size_t(8) * J * nparts * heap_stride(std::max<uint32_t>(K, 1))));
     CK(ctx->heap_cnt.ensure(4 * J * nparts));
     CK(ctx->hd.ensure(sizeof(double) * J * n));
     CK(ctx->hidx.ensure(sizeof(uint32_t) * J * n));

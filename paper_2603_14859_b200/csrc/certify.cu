@@ -216,7 +216,7 @@ __global__ void certify_reduce_kernel(const ReduceParams p, uint32_t Kp, uint32_
       } else if (p.heap_cnt[v] >= p.K) {
         float tmax = 0.0f;
         for (uint32_t a = lane; a < p.K; a += 32)
-          tmax = fmaxf(tmax, __uint_as_float(uint32_t(p.heap[v * p.K + a] >> 32)));
+          tmax = fmaxf(tmax, __uint_as_float(uint32_t(p.heap[v * heap_stride(p.K) + kHeapOff + a] >> 32)));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
         B = tmax;
@@ -229,7 +229,7 @@ __global__ void certify_reduce_kernel(const ReduceParams p, uint32_t Kp, uint32_
       uint32_t nc = 0;  // warp-uniform candidate count
       for (uint32_t q = 0; q < S; ++q) {
         const uint32_t cq = p.heap_cnt[v * S + q];
-        const unsigned long long* h = p.heap + (v * S + q) * p.K;
+        const unsigned long long* h = p.heap + (v * S + q) * heap_stride(p.K) + kHeapOff;
         for (uint32_t base = 0; base < cq; base += 32) {
           uint32_t a = base + lane;
           unsigned long long key = a < cq ? h[a] : ~0ull;

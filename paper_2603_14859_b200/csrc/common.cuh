@@ -235,7 +235,7 @@ struct ScanParams {
   const int* perm;      // [LP]
   const float* wsp;     // [LP]
   uint32_t K;           // heap capacity per voxel (top-n mode)
-  unsigned long long* heap;  // [J][K] keys (D32 bits << 32 | idx)
+  unsigned long long* heap;  // [J][nparts][heap_stride(K)] keys (D32 bits << 32 | idx), 8-ary heaps
   uint32_t* heap_cnt;   // [J]
   int prune;
   unsigned long long* work;  // frame-update counter (COUNT)
@@ -266,6 +266,10 @@ struct ScanParams {
   unsigned int* queue;      // work-queue counter (zeroed per run)
   const uint32_t* vorder;   // [J] voxel processed in slot j (tree mode) or nullptr (identity)
 };
+// Candidate heaps: 8-ary max-heaps; node i lives at slot i + kHeapOff of a (voxel, part) row of
+// heap_stride(K) keys, so the 8 children of node i (slots 8i + 8 .. 8i + 15) are one 64-B group.
+constexpr uint32_t kHeapOff = 7;
+__host__ __device__ inline uint32_t heap_stride(uint32_t K) { return (K + kHeapOff + 7u) & ~7u; }
 constexpr int kHyperSort = 256;  // max hyper-tiles per part (best-first order sorted in shared memory)
 constexpr int MOMW = 2 + 2 * ABC_MAX_P + 2;  // count, (S1,S2) x P, (KS1, KS2), pad
 cudaError_t launch_scan(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);
@@ -293,7 +297,7 @@ void launch_exact_scan(const ExactParams& p, cudaStream_t st);
 struct ReduceParams {
   // candidates
   int exact;                    // 1: candidates from the exact heap (no certification)
-  const unsigned long long* heap;  // fast mode: [J][nparts][K]
+  const unsigned long long* heap;  // fast mode: [J][nparts][heap_stride(K)]
   const uint32_t* heap_cnt;        // [J][nparts]
   uint32_t K;
   uint32_t nparts;

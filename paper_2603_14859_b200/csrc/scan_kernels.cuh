@@ -90,33 +90,38 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Max-heap of K keys (D32 bits << 32 | draw index) per voxel, in global memory.  A key above
-// the root of a full heap is ignored.  Returns (new count, new threshold bits).
-static __device__ __noinline__ uint2 heap_push(unsigned long long* h, uint32_t K, uint32_t cnt, unsigned long long key) {
+// 8-ary max-heap of K keys (D32 bits << 32 | draw index) per (voxel, part), in global memory
+// (layout: common.cuh heap_stride).  The caller pushes only keys below the root of a full heap
+// (D < taup).  A push touches <= 2 levels for K <= 72: one 64-B group of children per level.
+// Returns (new count, new threshold bits).
+static __device__ __noinline__ uint2 heap_push(unsigned long long* hb, uint32_t K, uint32_t cnt, unsigned long long key) {
+  unsigned long long* h = hb + kHeapOff;
   if (cnt < K) {
     uint32_t pos = cnt++;
     while (pos > 0) {
-      uint32_t par = (pos - 1) >> 1;
+      uint32_t par = (pos - 1) >> 3;
       unsigned long long pk = h[par];
       if (pk >= key) break;
       h[pos] = pk;
       pos = par;
     }
     h[pos] = key;
-  } else if (key < h[0]) {
+  } else {
     uint32_t pos = 0;
     for (;;) {
-      uint32_t l = 2 * pos + 1;
-      if (l >= K) break;
-      uint32_t c = l;
-      unsigned long long hc = h[l];
-      if (l + 1 < K) {
-        unsigned long long hr = h[l + 1];
-        if (hr > hc) { c = l + 1; hc = hr; }
-      }
-      if (hc <= key) break;
-      h[pos] = hc;
-      pos = c;
+      const uint32_t c0 = 8 * pos + 1;
+      if (c0 >= K) break;
+      const ulonglong2* g = reinterpret_cast<const ulonglong2*>(h + c0);
+      const ulonglong2 q0 = g[0], q1 = g[1], q2 = g[2], q3 = g[3];
+      const unsigned long long ch[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
+      unsigned long long m = 0;
+      uint32_t mj = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < 8; ++j)
+        if (c0 + j < K && ch[j] > m) { m = ch[j]; mj = j; }
+      if (m <= key) break;
+      h[pos] = m;
+      pos = c0 + mj;
     }
     h[pos] = key;
   }
@@ -306,7 +311,7 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
         if (!p.eps_mode) {
           unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
           if (COUNT && VPET_COUNT_PUSH) work += 1;
-          uint2 st = heap_push(p.heap + (uint64_t(V.vox[r]) * p.nparts + part) * p.K, p.K, V.cnt[r], key);
+          uint2 st = heap_push(p.heap + (uint64_t(V.vox[r]) * p.nparts + part) * heap_stride(p.K), p.K, V.cnt[r], key);
           V.cnt[r] = st.x;
           V.taup[r] = __uint_as_float(st.y);
           if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + V.vox[r], st.y);

@@ -8,8 +8,6 @@ from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": (),
-    "mb12": ("VPET_MBITS=12",),
-    "mb10": ("VPET_MBITS=10",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
