@@ -96,6 +96,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Returns (new count, new threshold bits).
 static __device__ __noinline__ uint2 heap_push(unsigned long long* hb, uint32_t K, uint32_t cnt, unsigned long long key) {
   unsigned long long* h = hb + kHeapOff;
+  unsigned long long root;
   if (cnt < K) {
     uint32_t pos = cnt++;
     while (pos > 0) {
@@ -106,8 +107,11 @@ static __device__ __noinline__ uint2 heap_push(unsigned long long* hb, uint32_t 
       pos = par;
     }
     h[pos] = key;
+    if (cnt < K) return make_uint2(cnt, 0x7f800000u);
+    root = pos == 0 ? key : h[0];  // heap just became full
   } else {
     uint32_t pos = 0;
+    root = key;
     for (;;) {
       const uint32_t c0 = 8 * pos + 1;
       if (c0 >= K) break;
@@ -120,13 +124,13 @@ static __device__ __noinline__ uint2 heap_push(unsigned long long* hb, uint32_t 
       for (uint32_t j = 0; j < 8; ++j)
         if (c0 + j < K && ch[j] > m) { m = ch[j]; mj = j; }
       if (m <= key) break;
+      if (pos == 0) root = m;  // the largest child of the root becomes the root
       h[pos] = m;
       pos = c0 + mj;
     }
     h[pos] = key;
   }
-  float tau = (cnt >= K) ? __uint_as_float(uint32_t(h[0] >> 32)) : __int_as_float(0x7f800000);
-  return make_uint2(cnt, __float_as_uint(tau));
+  return make_uint2(cnt, uint32_t(root >> 32));
 }
 
 // Exact FP64 discrepancy in acquisition order, operation for operation as the oracle.
