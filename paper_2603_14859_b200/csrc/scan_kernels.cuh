@@ -44,6 +44,15 @@ constexpr int NST = VPET_NST;  // TMA ring stages
 #endif
 constexpr int CH = VPET_CH;  // frames per pruning chunk (multiple of 4)
 constexpr int T = kTile;
+#ifndef VPET_REFRESH
+#define VPET_REFRESH 0  // pull tau_glob every VPET_REFRESH + 1 super-tiles
+#endif
+#ifndef VPET_HREFRESH
+#define VPET_HREFRESH 0  // and every VPET_HREFRESH + 1 hyper-tiles
+#endif
+#ifndef VPET_TREFRESH
+#define VPET_TREFRESH 2  // and before every evaluated tile (1: pipelined load, 2: immediate)
+#endif
 #ifndef VPET_SSORT
 #define VPET_SSORT 1
 #endif
@@ -342,6 +351,17 @@ __device__ __forceinline__ void refresh_tau(const ScanParams& p, Voxels<LP, R>& 
   }
 }
 
+// Software-pipelined variant: apply the value loaded at the previous call, issue the next load.
+template <int LP, int R>
+__device__ __forceinline__ void refresh_tau_pipe(const ScanParams& p, Voxels<LP, R>& V, float (&gpend)[R]) {
+  if (p.eps_mode || !p.tau_glob) return;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    V.tau[r] = fminf(V.tau[r], gpend[r]);
+    if (V.vox[r] < p.J) gpend[r] = __uint_as_float(__ldcg(p.tau_glob + V.vox[r]));
+  }
+}
+
 template <int LP, int R, int DIST>
 __device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const float* box, unsigned long long& work) {
   float2 acc[R];
@@ -610,9 +630,12 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
     best_first(hlb, uint32_t(nsub), okeys, horder, vis, tid);
 
     uint32_t it = 0;
+    float gpend[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) gpend[r] = __int_as_float(0x7f800000);
     for (uint32_t q = 0; q < nsub; ++q) {
       const uint64_t h = part + uint64_t(horder[q]) * S;
-      if ((q & 3) == 0) refresh_tau<LP, R>(p, V);
+      if ((q & VPET_HREFRESH) == 0) refresh_tau<LP, R>(p, V);
       const bool halive = box_alive<LP, R, DIST>(V, p.hbounds + h * 2 * LP, bwork);
       if (!__syncthreads_or(halive)) continue;
       const uint64_t s0 = h * p.hs;
@@ -627,7 +650,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       }
       for (uint32_t u = 0; u < ns; ++u, ++it) {
       const uint64_t s = s0 + (ssort ? sorder[u] : u);
-      if ((it & 7) == 7) refresh_tau<LP, R>(p, V);
+      if ((it & VPET_REFRESH) == VPET_REFRESH) refresh_tau<LP, R>(p, V);
       // super-tile bound
       bool alive = halive && box_alive<LP, R, DIST>(V, p.sbounds + s * 2 * LP, bwork);
       if (!__syncthreads_or(alive)) continue;
@@ -666,6 +689,8 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
         // phase is skipped), then only the warps whose lanes can improve evaluate the tile
         mbar_wait(&full[st], (g / NST) & 1u);
         if ((mym >> b) & 1u) {
+          if (VPET_TREFRESH == 1) refresh_tau_pipe<LP, R>(p, V, gpend);
+          if (VPET_TREFRESH == 2) refresh_tau<LP, R>(p, V);
           const float* sb = stage + size_t(st) * Shape<LP>::STAGE_FLOATS;
           const uint32_t* si = sidx + st * T;
           const uint64_t rem = N - t * T;

@@ -8,6 +8,8 @@ from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": (),
+    "tref0": ("VPET_TREFRESH=0",),
+    "tref2": ("VPET_TREFRESH=2",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
