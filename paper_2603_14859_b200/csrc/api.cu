@@ -501,8 +501,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
   // draw-range split of the tree scan (interleaved super-tiles): balances heavy voxels over SMs
   uint32_t nparts = 1;
-  if (tree && !eps) nparts = K <= 64 ? 4u : (K <= 512 ? 2u : 1u);
-  if (tree && eps) nparts = 4u;
+  if (tree && !eps) nparts = K <= 512 ? 6u : 2u;
+  if (tree && eps) nparts = 6u;
   if (const char* e = getenv("VPET_NPARTS")) nparts = uint32_t(std::max(1, atoi(e)));  // tuning knob
   // hyper-tiles of hs super-tiles: the unit of the work split and of the best-first order; at most
   // kHyperSort per part
