@@ -77,7 +77,7 @@ struct abc_ctx {
   // device tables
   bool dirty = true;
   uint32_t G = 0, GF = 0;
-  DevBuf d_fdur, d_fs, d_fe, d_favg, d_w, d_wsc, d_gt, d_gc, d_gframe, d_ft, d_fc, d_fframe;
+  DevBuf d_fdur, d_fs, d_fe, d_favg, d_w, d_wsc, d_gt, d_gc, d_gframe, d_gcode, d_ft, d_fc, d_fframe;
   // work buffers
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
   DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, hbounds, tau_glob, queue;
@@ -209,6 +209,30 @@ abc_status build_tables(abc_ctx* ctx) {
   CK(upload(ctx->d_gt, gt));
   CK(upload(ctx->d_gc, gc));
   CK(upload(ctx->d_gframe, gfr));
+  {  // phi cache codes: an LRU of kPhiSlots segment lengths, simulated here (the grid is shared)
+    std::vector<uint8_t> code(gt.size() > 1 ? gt.size() - 1 : 1, 0x80);
+    double slot_h[kPhiSlots];
+    int age[kPhiSlots];
+    for (int c = 0; c < kPhiSlots; ++c) { slot_h[c] = -1.0; age[c] = -1; }
+    for (size_t k = 0; k + 1 < gt.size(); ++k) {
+      const double h = gt[k + 1] - gt[k];  // the device computes the same difference
+      int hit = -1;
+      for (int c = 0; c < kPhiSlots; ++c)
+        if (slot_h[c] == h) hit = c;
+      if (hit >= 0) {
+        code[k] = uint8_t(hit);
+      } else {
+        int v = 0;
+        for (int c = 1; c < kPhiSlots; ++c)
+          if (age[c] < age[v]) v = c;
+        slot_h[v] = h;
+        hit = v;
+        code[k] = uint8_t(0x80 | v);
+      }
+      age[hit] = int(k);
+    }
+    CK(upload(ctx->d_gcode, code));
+  }
   CK(upload(ctx->d_ft, ft));
   CK(upload(ctx->d_fc, fc));
   CK(upload(ctx->d_fframe, ffr));
@@ -233,6 +257,7 @@ Tables make_tables(const abc_ctx* c, uint32_t LS) {
   T.gt = c->d_gt.as<double>();
   T.gc = c->d_gc.as<double>();
   T.gframe = c->d_gframe.as<int>();
+  T.gcode = c->d_gcode.as<uint8_t>();
   T.GF = c->GF;
   T.ft = c->d_ft.as<double>();
   T.fc = c->d_fc.as<double>();
@@ -879,7 +904,7 @@ void abc_destroy(abc_ctx* ctx) {
                      &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
-                    &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,
+                    &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,
                     &ctx->bank,   &ctx->bankp, &ctx->var,    &ctx->perm,   &ctx->wsp,        &ctx->heap,
                     &ctx->heap_cnt, &ctx->tacs, &ctx->fb_list, &ctx->fb_len, &ctx->work,     &ctx->hd,
                     &ctx->hidx,   &ctx->mom,   &ctx->flag,   &ctx->outs};

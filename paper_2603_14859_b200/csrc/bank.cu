@@ -29,6 +29,7 @@ struct FrameAcc {
 __device__ void sim_2tcm_pwl(const Tables& T, double a1, double a2, double c1, double c2, double Vb,
                              float* out) {
   double I1 = 0.0, I2 = 0.0;
+  Phi P0{}, P1{}, Q0{}, Q1{};
   FrameAcc fa;
   auto flush = [&](int f) {
     double v = ((1.0 - Vb) * (c1 * fa.A + c2 * fa.B) + Vb * T.favg_in[f]) / T.fdur[f];
@@ -39,8 +40,16 @@ __device__ void sim_2tcm_pwl(const Tables& T, double a1, double a2, double c1, d
     double h = t1 - t0;
     double ck = T.gc[k], ck1 = T.gc[k + 1];
     int f = T.gframe[k];
-    Phi p = phi_all(a1 * h);
-    Phi q = phi_all(a2 * h);
+    // phi(a h) depends on the draw only through a: reuse it across segments of equal length h
+    // (bit-identical to recomputing; the cache schedule is the same for every draw)
+    const uint32_t code = T.gcode[k];
+    const uint32_t slot = code & 3u;
+    if (code & 0x80u) {
+      Phi np = phi_all(a1 * h), nq = phi_all(a2 * h);
+      if (slot == 0) { P0 = np; Q0 = nq; } else { P1 = np; Q1 = nq; }
+    }
+    const Phi& p = slot == 0 ? P0 : P1;
+    const Phi& q = slot == 0 ? Q0 : Q1;
     double dc = ck1 - ck;
     double s1 = h * p.p1 * I1 + h * h * (ck1 * p.ps - dc * p.om);
     double s2 = h * q.p1 * I2 + h * h * (ck1 * q.ps - dc * q.om);
@@ -104,12 +113,19 @@ __device__ void sim_mrtm(const Tables& T, double R1, double k2, double k2a, floa
   double I = 0.0;
   FrameAcc fa;
   double kf = k2 - R1 * k2a;
+  Phi P0{}, P1{};
   auto flush = [&](int f) { out[f] = __double2float_rn((R1 * T.favg_in[f] + kf * fa.A) / T.fdur[f]); };
   for (uint32_t k = 0; k + 1 < T.G; ++k) {
     double h = T.gt[k + 1] - T.gt[k];
     double ck = T.gc[k], ck1 = T.gc[k + 1];
     int f = T.gframe[k];
-    Phi p = phi_all(k2a * h);
+    const uint32_t code = T.gcode[k];
+    const uint32_t slot = code & 3u;
+    if (code & 0x80u) {
+      Phi np = phi_all(k2a * h);
+      if (slot == 0) P0 = np; else P1 = np;
+    }
+    const Phi& p = slot == 0 ? P0 : P1;
     double s = h * p.p1 * I + h * h * (ck1 * p.ps - (ck1 - ck) * p.om);
     if (f != fa.cur) {
       if (fa.cur >= 0) flush(fa.cur);

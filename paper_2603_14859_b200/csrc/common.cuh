@@ -136,6 +136,7 @@ __device__ inline double phi1_only(double x) { return x == 0.0 ? 1.0 : -expm1(-x
 // ---------------------------------------------------------------------------------------
 // Launch-side helpers
 // ---------------------------------------------------------------------------------------
+constexpr int kPhiSlots = 2;  // per-rate cache of phi(a h) for recently seen segment lengths h
 struct Tables {
   // frames (acquisition order)
   uint32_t L, LS;          // frames, padded stride of the exact bank
@@ -149,6 +150,7 @@ struct Tables {
   const double* gt;        // [G]
   const double* gc;        // [G] input value at grid points
   const int* gframe;       // [G-1] frame of segment k or -1
+  const uint8_t* gcode;    // [G-1] phi cache code of segment k: bit 7 = recompute, bits 0-1 = slot
   // fine grid (lp-ntPET)
   uint32_t GF;
   const double* ft;
