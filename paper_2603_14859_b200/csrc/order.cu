@@ -166,36 +166,57 @@ __device__ __forceinline__ float ord2f(unsigned int u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
 
-__device__ __forceinline__ void project(const OrderParams& p, uint64_t i, const float* sm_mu, const float* sm_pc,
-                                        const int* sm_perm, const float* sm_wsp, float pr[kNPC]) {
-  const float* row = p.bank + i * p.LS;
+// Projection of bank rows on the principal axes, in acquisition frame order (float4 row loads):
+// pr_c = sum_f bank[i][f] coef[c][f] - off[c], coef[c][perm[k]] = wsp[k] pc[c][k],
+// off[c] = sum_k mean[perm[k]] pc[c][k].  (A heuristic ordering key: exactness does not depend on it.)
+struct ProjSmem {
+  float coef[kNPC][kMaxLP];
+  float off[kNPC];
+};
+
+__device__ void proj_setup(const OrderParams& p, ProjSmem& s) {
+  for (uint32_t e = threadIdx.x; e < kNPC * kMaxLP; e += blockDim.x) (&s.coef[0][0])[e] = 0.0f;
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    const int src = p.perm[k];
+    if (src >= 0)
+      for (int c = 0; c < kNPC; ++c) s.coef[c][src] = p.wsp[k] * p.pcs[c * p.LP + k];
+  }
+  if (threadIdx.x < kNPC) {
+    float o = 0.0f;
+    for (uint32_t k = 0; k < p.LP; ++k)
+      if (p.perm[k] >= 0) o = fmaf(float(p.mean[p.perm[k]]), p.pcs[threadIdx.x * p.LP + k], o);
+    s.off[threadIdx.x] = o;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void project(const OrderParams& p, const ProjSmem& s, uint64_t i, float pr[kNPC]) {
+  const float4* row = reinterpret_cast<const float4*>(p.bank + i * p.LS);
 #pragma unroll
-  for (int c = 0; c < kNPC; ++c) pr[c] = 0.0f;
-  for (uint32_t k = 0; k < p.LP; ++k) {
-    int src = sm_perm[k];
-    if (src < 0) break;
-    float x = sm_wsp[k] * __ldg(row + src) - sm_mu[k];
+  for (int c = 0; c < kNPC; ++c) pr[c] = -s.off[c];
+  for (uint32_t q = 0; q < p.LS / 4; ++q) {
+    const float4 x = __ldg(row + q);
 #pragma unroll
-    for (int c = 0; c < kNPC; ++c) pr[c] = fmaf(x, sm_pc[c * p.LP + k], pr[c]);
+    for (int c = 0; c < kNPC; ++c) {
+      const float* cf = s.coef[c] + 4 * q;
+      pr[c] = fmaf(x.x, cf[0], pr[c]);
+      pr[c] = fmaf(x.y, cf[1], pr[c]);
+      pr[c] = fmaf(x.z, cf[2], pr[c]);
+      pr[c] = fmaf(x.w, cf[3], pr[c]);
+    }
   }
 }
 
 __global__ void __launch_bounds__(256) proj_minmax_kernel(const OrderParams p) {
-  __shared__ float sm_mu[kMaxLP], sm_wsp[kMaxLP], sm_pc[kNPC * kMaxLP];
-  __shared__ int sm_perm[kMaxLP];
-  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
-    sm_perm[k] = p.perm[k];
-    sm_wsp[k] = p.wsp[k];
-    sm_mu[k] = p.perm[k] >= 0 ? float(p.mean[p.perm[k]]) : 0.0f;
-  }
-  for (uint32_t e = threadIdx.x; e < kNPC * p.LP; e += blockDim.x) sm_pc[e] = p.pcs[e];
-  __syncthreads();
+  __shared__ ProjSmem sm;
+  proj_setup(p, sm);
   float lo[kNPC], hi[kNPC];
 #pragma unroll
   for (int c = 0; c < kNPC; ++c) { lo[c] = 3.0e38f; hi[c] = -3.0e38f; }
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.N; i += uint64_t(gridDim.x) * blockDim.x) {
     float pr[kNPC];
-    project(p, i, sm_mu, sm_pc, sm_perm, sm_wsp, pr);
+    project(p, sm, i, pr);
 #pragma unroll
     for (int c = 0; c < kNPC; ++c) { lo[c] = fminf(lo[c], pr[c]); hi[c] = fmaxf(hi[c], pr[c]); }
   }
@@ -233,15 +254,9 @@ __device__ __forceinline__ unsigned long long spread4(unsigned long long x) {
 }
 
 __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
-  __shared__ float sm_mu[kMaxLP], sm_wsp[kMaxLP], sm_pc[kNPC * kMaxLP];
-  __shared__ int sm_perm[kMaxLP];
+  __shared__ ProjSmem sm;
   __shared__ float sm_lo[kNPC], sm_scale;
-  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
-    sm_perm[k] = p.perm[k];
-    sm_wsp[k] = p.wsp[k];
-    sm_mu[k] = p.perm[k] >= 0 ? float(p.mean[p.perm[k]]) : 0.0f;
-  }
-  for (uint32_t e = threadIdx.x; e < kNPC * p.LP; e += blockDim.x) sm_pc[e] = p.pcs[e];
+  proj_setup(p, sm);
   if (threadIdx.x == 0) {
     float rng = 0.0f;
     for (int c = 0; c < kNPC; ++c) {
@@ -253,7 +268,7 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
   __syncthreads();
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.N; i += uint64_t(gridDim.x) * blockDim.x) {
     float pr[kNPC];
-    project(p, i, sm_mu, sm_pc, sm_perm, sm_wsp, pr);
+    project(p, sm, i, pr);
     unsigned long long key = 0;
 #pragma unroll
     for (int c = 0; c < kNPC; ++c) {
@@ -266,42 +281,60 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
   }
 }
 
-// ---- scan-order copy: bankp[j][k] = -(wsp[k] * bank[order[j]][perm[k]]), idxmap[j] = order[j] ----
-__global__ void __launch_bounds__(256) permute_kernel(const OrderParams p) {
+// ---- scan-order copy fused with the tile bounds, one warp per tile of kTile rows:
+// bankp[j][k] = -(wsp[k] * bank[order[j]][perm[k]]), idxmap[j] = order[j], and (tree mode)
+// tbounds[t] = per-frame [min, max] of the tile's bankp rows.  Raw rows are gathered with
+// coalesced 16-B loads into shared memory, then written out frame-contiguous. ----
+constexpr int kPermWarps = 4;
+__global__ void __launch_bounds__(32 * kPermWarps) permute_kernel(const OrderParams p) {
+  extern __shared__ float psm[];  // [kPermWarps][kTile][LS + 1]
   __shared__ int sperm[kMaxLP];
   __shared__ float swsp[kMaxLP];
+  __shared__ uint32_t sidx[kPermWarps][kTile];
   for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
     sperm[k] = p.perm[k];
     swsp[k] = p.wsp[k];
   }
   __syncthreads();
-  uint64_t total = p.N * p.LP;
-  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += uint64_t(gridDim.x) * blockDim.x) {
-    uint64_t j = e / p.LP;
-    uint32_t k = uint32_t(e - j * p.LP);
-    uint64_t i = p.order ? p.order[j] : j;
-    int src = sperm[k];
-    float v = 0.0f;
-    if (src >= 0) v = -__fmul_rn(swsp[k], __ldg(p.bank + i * p.LS + src));
-    p.bankp[e] = v;
-    if (k == 0 && p.idxmap) p.idxmap[j] = uint32_t(i);
-  }
-}
-
-// ---- tile bounds: per tile of T rows and per frame, min and max of bankp ----
-__global__ void __launch_bounds__(128) tile_bounds_kernel(const OrderParams p) {
-  uint64_t t = blockIdx.x;
-  uint64_t r0 = t * kTile;
-  uint64_t r1 = r0 + kTile < p.N ? r0 + kTile : p.N;
-  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
-    float lo = 3.0e38f, hi = -3.0e38f;
-    for (uint64_t j = r0; j < r1; ++j) {
-      float v = p.bankp[j * p.LP + k];
-      lo = fminf(lo, v);
-      hi = fmaxf(hi, v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t LS = p.LS, Q = LS / 4, stride = LS + 1;
+  float* rows = psm + size_t(wid) * kTile * stride;
+  const uint64_t ntile = (p.N + kTile - 1) / kTile;
+  for (uint64_t t = uint64_t(blockIdx.x) * kPermWarps + wid; t < ntile; t += uint64_t(gridDim.x) * kPermWarps) {
+    const uint64_t j0 = t * kTile;
+    const uint32_t nr = uint32_t((p.N - j0) < uint64_t(kTile) ? (p.N - j0) : uint64_t(kTile));
+    uint32_t myi = 0;
+    if (uint32_t(lane) < nr) {
+      myi = p.order ? p.order[j0 + lane] : uint32_t(j0 + lane);
+      if (p.idxmap) p.idxmap[j0 + lane] = myi;
     }
-    p.tbounds[(t * 2 + 0) * p.LP + k] = lo;
-    p.tbounds[(t * 2 + 1) * p.LP + k] = hi;
+    sidx[wid][lane] = myi;
+    __syncwarp();
+    for (uint32_t e = lane; e < nr * Q; e += 32) {  // gather: element e = (row e / Q, float4 e % Q)
+      const uint32_t r = e / Q, q = e % Q;
+      const float4 x = __ldg(reinterpret_cast<const float4*>(p.bank + uint64_t(sidx[wid][r]) * LS) + q);
+      float* d = rows + r * stride + 4 * q;
+      d[0] = x.x; d[1] = x.y; d[2] = x.z; d[3] = x.w;
+    }
+    __syncwarp();
+    for (uint32_t k0 = 0; k0 < p.LP; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const bool on = k < p.LP;
+      const int src = on ? sperm[k] : -1;
+      const float ws = on ? swsp[k] : 0.0f;
+      float lo = 3.0e38f, hi = -3.0e38f;
+      for (uint32_t r = 0; r < nr; ++r) {
+        const float v = src >= 0 ? -__fmul_rn(ws, rows[r * stride + src]) : 0.0f;
+        if (on) p.bankp[(j0 + r) * p.LP + k] = v;
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+      }
+      if (on && p.tree && p.tbounds) {
+        p.tbounds[(t * 2 + 0) * p.LP + k] = lo;
+        p.tbounds[(t * 2 + 1) * p.LP + k] = hi;
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -450,15 +483,22 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
   } else {
     q.order = nullptr;
   }
-  permute_kernel<<<148 * 8, 256, 0, st>>>(q);
-  *launches += 1;
+  {
+    const size_t psmem = sizeof(float) * kPermWarps * kTile * (p.LS + 1);
+    static size_t attr = 0;
+    if (psmem > 48 * 1024 && psmem > attr) {
+      cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(psmem));
+      attr = psmem;
+    }
+    permute_kernel<<<148 * 8, 32 * kPermWarps, psmem, st>>>(q);
+    *launches += 1;
+  }
   if (p.tree) {
     uint64_t ntile = (p.N + kTile - 1) / kTile;
     uint64_t nsup = (ntile + kSuper - 1) / kSuper;
-    tile_bounds_kernel<<<unsigned(ntile), 128, 0, st>>>(p);
     super_bounds_kernel<<<unsigned(nsup), 128, 0, st>>>(p, ntile);
     hyper_bounds_kernel<<<unsigned(p.nhyper), 128, 0, st>>>(p, nsup);
-    *launches += 3;
+    *launches += 2;
   }
   return cudaGetLastError();
 }
