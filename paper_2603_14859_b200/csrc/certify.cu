@@ -74,6 +74,87 @@ __device__ void warp_sort_keys(double* key, uint32_t n2, int lane) {
   }
 }
 
+// Register bitonic sorts of 32 * E elements (element g = e * 32 + lane), ascending.
+template <int E, bool PAIRS>
+__device__ __forceinline__ void warp_sort_reg(double (&k)[E], uint32_t (&ix)[E], int lane) {
+#pragma unroll
+  for (uint32_t size = 2; size <= 32u * E; size <<= 1) {
+#pragma unroll
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const uint32_t es = stride / 32;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int e2 = e ^ int(es);
+          if (e2 > e) {
+            const uint32_t g = uint32_t(e) * 32 + lane;
+            const bool asc = (g & size) == 0;
+            const bool gt = PAIRS ? pair_gt(k[e], ix[e], k[e2], ix[e2]) : (k[e] > k[e2]);
+            if (gt == asc) {
+              double t = k[e]; k[e] = k[e2]; k[e2] = t;
+              uint32_t u = ix[e]; ix[e] = ix[e2]; ix[e2] = u;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint32_t g = uint32_t(e) * 32 + lane;
+          const double ok = __shfl_xor_sync(0xffffffffu, k[e], stride);
+          const uint32_t oi = __shfl_xor_sync(0xffffffffu, ix[e], stride);
+          const bool lower = (lane & stride) == 0;
+          const bool asc = (g & size) == 0;
+          // the lower position keeps the smaller element when ascending
+          const bool mine_gt = PAIRS ? pair_gt(k[e], ix[e], ok, oi) : (k[e] > ok);
+          const bool other_gt = PAIRS ? pair_gt(ok, oi, k[e], ix[e]) : (ok > k[e]);
+          const bool take = (lower == asc) ? mine_gt : other_gt;
+          if (take) { k[e] = ok; ix[e] = oi; }
+        }
+      }
+    }
+  }
+}
+
+// Sort n2 (power of two) smem keys (and indices if idx) ascending: registers for n2 <= 64.
+__device__ void warp_sort_any(double* key, uint32_t* idx, uint32_t n2, int lane) {
+  if (n2 <= 32) {
+    double k[1];
+    uint32_t ix[1];
+    const bool in = uint32_t(lane) < n2;
+    k[0] = in ? key[lane] : __longlong_as_double(0x7ff0000000000000ll);
+    ix[0] = (in && idx) ? idx[lane] : 0xffffffffu;
+    __syncwarp();
+    if (idx) warp_sort_reg<1, true>(k, ix, lane);
+    else warp_sort_reg<1, false>(k, ix, lane);
+    if (in) {  // padding (+inf, 0xffffffff) sorts last and is never stored back
+      key[lane] = k[0];
+      if (idx) idx[lane] = ix[0];
+    }
+    __syncwarp();
+  } else if (n2 == 64) {
+    double k[2];
+    uint32_t ix[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      k[e] = key[e * 32 + lane];
+      ix[e] = idx ? idx[e * 32 + lane] : 0u;
+    }
+    __syncwarp();
+    if (idx) warp_sort_reg<2, true>(k, ix, lane);
+    else warp_sort_reg<2, false>(k, ix, lane);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      key[e * 32 + lane] = k[e];
+      if (idx) idx[e * 32 + lane] = ix[e];
+    }
+    __syncwarp();
+  } else if (idx) {
+    warp_sort_pairs(key, idx, n2, lane);
+  } else {
+    warp_sort_keys(key, n2, lane);
+  }
+}
+
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -123,6 +204,16 @@ __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* c
   const uint32_t c = cnt[pref];
   const bool tcm = kind <= ABC_2TCM_REV;
   const float NANF = __int_as_float(0x7fc00000);
+  // n <= 32: each lane draws the parameters of its accepted draw once, for all columns
+  const bool small = n <= 32;
+  float thr[ABC_MAX_P];
+  bool mine0 = false;
+  uint32_t bal0 = 0;
+  if (small) {
+    mine0 = uint32_t(lane) < n && model_index(p.prior, ci[lane]) == pref;
+    if (mine0) draw_theta(p.prior, ci[lane], thr);
+    bal0 = __ballot_sync(0xffffffffu, mine0);
+  }
   for (uint32_t k = 0; k <= p.P; ++k) {  // column P = K_i
     const bool is_ki = (k == p.P);
     if (is_ki && !tcm) {
@@ -138,7 +229,15 @@ __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* c
     if (exists) {
       uint32_t npos = 0;
       double sum = 0.0;
-      for (uint32_t base = 0; base < n; base += 32) {
+      if (small) {
+        if (mine0) {
+          double x = is_ki ? double(thr[0]) * double(thr[2]) / (double(thr[1]) + double(thr[2])) : double(thr[k]);
+          sc[__popc(bal0 & ((1u << lane) - 1u))] = x;
+          sum += x;
+        }
+        npos = __popc(bal0);
+      }
+      for (uint32_t base = 0; !small && base < n; base += 32) {
         uint32_t a = base + lane;
         bool mine = a < n && model_index(p.prior, ci[a]) == pref;
         uint32_t bal = __ballot_sync(0xffffffffu, mine);
@@ -160,7 +259,7 @@ __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* c
       ss = warp_sum(ss);
       for (uint32_t a = c + lane; a < np2; a += 32) sc[a] = __longlong_as_double(0x7ff0000000000000ll);
       __syncwarp();
-      warp_sort_keys(sc, np2, lane);
+      warp_sort_any(sc, nullptr, np2, lane);
       mean = float(mu);
       sd = c >= 2 ? float(sqrt(ss / double(c - 1))) : NANF;
       q3[0] = float(quantile7(sc, c, 0.025));
@@ -262,7 +361,7 @@ __global__ void certify_reduce_kernel(const ReduceParams p, uint32_t Kp, uint32_
     {
       uint32_t kp = 32;  // sort only the occupied power of two
       while (kp < cnt) kp <<= 1;
-      warp_sort_pairs(cd, ci, kp < Kp ? kp : Kp, lane);
+      warp_sort_any(cd, ci, kp < Kp ? kp : Kp, lane);
     }
     if (!p.exact && tK < __int_as_float(0x7f800000)) {
       double Y2 = 0.0, Y1 = 0.0;
