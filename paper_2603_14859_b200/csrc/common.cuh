@@ -15,7 +15,7 @@ constexpr int kNPC = 4;      // principal axes used for the draw order (order.cu
 #define VPET_TILE 32
 #endif
 #ifndef VPET_SUPER
-#define VPET_SUPER 32
+#define VPET_SUPER 8
 #endif
 constexpr int kTile = VPET_TILE;    // draws per tile (bounding box + TMA transfer unit)
 constexpr int kSuper = VPET_SUPER;  // tiles per super-tile (<= 32: one bit per tile in a mask)
@@ -272,7 +272,10 @@ struct ScanParams {
 // heap_stride(K) keys, so the 8 children of node i (slots 8i + 8 .. 8i + 15) are one 64-B group.
 constexpr uint32_t kHeapOff = 7;
 __host__ __device__ inline uint32_t heap_stride(uint32_t K) { return (K + kHeapOff + 7u) & ~7u; }
-constexpr int kHyperSort = 256;  // max hyper-tiles per part (best-first order sorted in shared memory)
+#ifndef VPET_HSORTMAX
+#define VPET_HSORTMAX 256
+#endif
+constexpr int kHyperSort = VPET_HSORTMAX;  // max hyper-tiles per part (best-first order sorted in shared memory)
 constexpr int MOMW = 2 + 2 * ABC_MAX_P + 2;  // count, (S1,S2) x P, (KS1, KS2), pad
 cudaError_t launch_scan(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);
 cudaError_t launch_scan_wl2(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st);

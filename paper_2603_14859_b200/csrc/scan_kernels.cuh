@@ -53,6 +53,9 @@ constexpr int T = kTile;
 #ifndef VPET_TREFRESH
 #define VPET_TREFRESH 2  // and before every evaluated tile (1: pipelined load, 2: immediate)
 #endif
+#ifndef VPET_RREFRESH
+#define VPET_RREFRESH 0  // and every VPET_RREFRESH rows inside a tile (0: off)
+#endif
 #ifndef VPET_SSORT
 #define VPET_SSORT 1
 #endif
@@ -695,7 +698,10 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
           const uint32_t* si = sidx + st * T;
           const uint64_t rem = N - t * T;
           const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
-          for (uint32_t d = 0; d < nd; ++d) eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, si[d], part, work);
+          for (uint32_t d = 0; d < nd; ++d) {
+            if (VPET_RREFRESH && d > 0 && (d % VPET_RREFRESH) == 0) refresh_tau<LP, R>(p, V);
+            eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, si[d], part, work);
+          }
         }
         __syncwarp();
         if (lane == 0) {

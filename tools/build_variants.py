@@ -7,9 +7,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
-    "base": (),
-    "tref0": ("VPET_TREFRESH=0",),
-    "tref2": ("VPET_TREFRESH=2",),
+    "super8": ("VPET_SUPER=8",),
+    "super8h512": ("VPET_SUPER=8", "VPET_HSORTMAX=512"),
+    "super4": ("VPET_SUPER=4",),
+    "super4h512": ("VPET_SUPER=4", "VPET_HSORTMAX=512"),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
