@@ -34,13 +34,13 @@ namespace scan {
 #define VPET_NT 64
 #endif
 #ifndef VPET_NST
-#define VPET_NST 3
+#define VPET_NST 2
 #endif
 constexpr int NT = VPET_NT;   // threads per CTA (the warps of a CTA share tile loads)
 constexpr int NW = NT / 32;
 constexpr int NST = VPET_NST;  // TMA ring stages
 #ifndef VPET_CH
-#define VPET_CH 12
+#define VPET_CH 16
 #endif
 constexpr int CH = VPET_CH;  // frames per pruning chunk (multiple of 4)
 constexpr int T = kTile;

@@ -7,10 +7,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
-    "super8": ("VPET_SUPER=8",),
-    "super8h512": ("VPET_SUPER=8", "VPET_HSORTMAX=512"),
-    "super4": ("VPET_SUPER=4",),
-    "super4h512": ("VPET_SUPER=4", "VPET_HSORTMAX=512"),
+    "base": (),
+    "ch16": ("VPET_CH=16",),
+    "nst2": ("VPET_NST=2",),
+    "ch16nst2": ("VPET_CH=16", "VPET_NST=2"),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
