@@ -69,8 +69,12 @@ struct Shape {
   static constexpr int MINB = ((LP * R <= 96) ? 16 : 8) / NW;
 #endif
   static constexpr size_t STAGE_FLOATS = size_t(T) * LP;
+  // prefetched boxes of one super-tile: its own [lo; hi] then its kSuper tiles' (double buffered)
+  static constexpr size_t BOXB_FLOATS = size_t(kSuper + 1) * 2 * LP;
   static constexpr size_t SMEM = size_t(NST) * (STAGE_FLOATS * 4 + T * 4) + NST * 8 + NST * 4 +
-                                 NW * 4 + NW * LP * 4 + 16 + 64 + size_t(kHyperSort) * (NW * 8 + 8 + NW * 4) + kHyperSort / 8;
+                                 NW * 4 + NW * LP * 4 + 16 + 64 + size_t(kHyperSort) * (NW * 8 + 8 + NW * 4) + kHyperSort / 8 +
+                                 2 * BOXB_FLOATS * 4 + 16 + 16;
+
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
@@ -259,8 +263,9 @@ __device__ __forceinline__ void bound_chunk(const Voxels<LP, R>& V, const float*
                                             float2 (&acc)[R]) {
 #pragma unroll
   for (int q = C * CH; q < ((C + 1) * CH < LP ? (C + 1) * CH : LP); q += 4) {
-    const float4 l4 = __ldg(reinterpret_cast<const float4*>(lo + q));
-    const float4 h4 = __ldg(reinterpret_cast<const float4*>(hi + q));
+    // generic loads: the boxes live in shared memory (prefetched super/tile boxes) or global memory
+    const float4 l4 = *reinterpret_cast<const float4*>(lo + q);
+    const float4 h4 = *reinterpret_cast<const float4*>(hi + q);
     const float2 la = make_float2(l4.x, l4.y), lc = make_float2(l4.z, l4.w);
     const float2 ha = make_float2(h4.x, h4.y), hc = make_float2(h4.z, h4.w);
 #pragma unroll
@@ -556,6 +561,10 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
   uint32_t* sorder = horder + kHyperSort;                                  // [kHyperSort] super-tile order
   uint32_t* vis = sorder + kHyperSort;                                     // [kHyperSort / 32]
   float* hlb = reinterpret_cast<float*>(vis + kHyperSort / 32);            // [NW][kHyperSort]
+  constexpr size_t BXF = Shape<LP>::BOXB_FLOATS;
+  float* bbuf = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(hlb + NW * kHyperSort) + 15) & ~uintptr_t(15));  // [2][BXF]
+  uint64_t* bbar = reinterpret_cast<uint64_t*>(bbuf + 2 * BXF);                  // [2]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t N = p.N;
@@ -574,8 +583,20 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       mbar_init(&full[s], 1);
       arrivals[s] = 0;
     }
+    mbar_init(&bbar[0], 1);
+    mbar_init(&bbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  uint32_t bcount = 0;  // super-tile box buffers consumed (CTA-uniform)
+  auto prefetch_boxes = [&](uint64_t sx, uint32_t b) {
+    const uint64_t a0 = sx * kSuper;
+    const uint64_t a1 = (a0 + kSuper < p.ntile) ? a0 + kSuper : p.ntile;
+    const uint32_t sbytes = 2 * LP * 4, tbytes = uint32_t(a1 - a0) * 2 * LP * 4;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&bbar[b], sbytes + tbytes);
+    bulk_g2s(bbuf + b * BXF, p.sbounds + sx * 2 * LP, sbytes, &bbar[b]);
+    bulk_g2s(bbuf + b * BXF + 2 * LP, p.tbounds + a0 * 2 * LP, tbytes, &bbar[b]);
+  };
   const uint32_t S = p.nparts;
   const uint64_t nvt = (p.J + uint64_t(NT) * R - 1) / (uint64_t(NT) * R);
   const uint64_t nitems = nvt * S;
@@ -653,9 +674,18 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       }
       for (uint32_t u = 0; u < ns; ++u, ++it) {
       const uint64_t s = s0 + (ssort ? sorder[u] : u);
+      // boxes of this super-tile (and its tiles) arrive by TMA; the next one's are requested now
+      const uint32_t cur = bcount & 1u;
+      if (tid == 0) {
+        if (u == 0) prefetch_boxes(s, cur);
+        if (u + 1 < ns) prefetch_boxes(s0 + (ssort ? sorder[u + 1] : u + 1), cur ^ 1u);
+      }
       if ((it & VPET_REFRESH) == VPET_REFRESH) refresh_tau<LP, R>(p, V);
+      mbar_wait(&bbar[cur], (bcount >> 1) & 1u);
+      ++bcount;
+      const float* sbx = bbuf + cur * BXF;
       // super-tile bound
-      bool alive = halive && box_alive<LP, R, DIST>(V, p.sbounds + s * 2 * LP, bwork);
+      bool alive = halive && box_alive<LP, R, DIST>(V, sbx, bwork);
       if (!__syncthreads_or(alive)) continue;
       // tile bounds -> per-warp masks
       const uint64_t t0 = s * kSuper;
@@ -663,7 +693,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       uint32_t mask = 0;
       if (alive) {
         for (uint64_t t = t0; t < t1; ++t)
-          if (box_alive<LP, R, DIST>(V, p.tbounds + t * 2 * LP, bwork)) mask |= 1u << uint32_t(t - t0);
+          if (box_alive<LP, R, DIST>(V, sbx + 2 * LP + (t - t0) * 2 * LP, bwork)) mask |= 1u << uint32_t(t - t0);
       }
       if (lane == 0) wmask[wid] = mask;
       __syncthreads();
