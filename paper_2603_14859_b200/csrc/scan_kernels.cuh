@@ -328,6 +328,11 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       float D = __fadd_rn(acc[r].x, acc[r].y);
+#ifndef VPET_PUSHCHECK
+#define VPET_PUSHCHECK 0  // re-read the shared threshold before a heap push
+#endif
+      if (VPET_PUSHCHECK && D < V.tau[r] && !p.eps_mode && p.tau_glob)
+        V.tau[r] = fminf(V.tau[r], __uint_as_float(__ldcg(p.tau_glob + V.vox[r])));
       if (D < V.tau[r]) {
         if (!p.eps_mode) {
           unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);

@@ -8,9 +8,7 @@ from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": (),
-    "ch16": ("VPET_CH=16",),
-    "nst2": ("VPET_NST=2",),
-    "ch16nst2": ("VPET_CH=16", "VPET_NST=2"),
+    "nopc": ("VPET_PUSHCHECK=0",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
