@@ -221,8 +221,8 @@ NOISE_CV = {"low": 0.02, "mid": 0.05, "high": 0.10}
 
 
 def config2(J=10_000, N_per_model=100_000, n=100, noise="mid", seed=1002, abc_seed=2026, device="cpu",
-            distance="WL2", lpnt_step_min=0.05):
-    start, dur = uniform_frames(61, 60.0)
+            distance="WL2", lpnt_step_min=0.05, n_frames=61):
+    start, dur = uniform_frames(n_frames, 60.0)
     rng = np.random.default_rng(seed)
     half = J // 2
     R1 = rng.uniform(0.8, 1.2, J)

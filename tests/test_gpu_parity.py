@@ -119,6 +119,40 @@ def test_eps_mode(cfg1):
     compare(g2, o2, topn=False)
 
 
+def test_wide_schedule_lp128():
+    """L = 100 frames: the widest scan layout (LP = 128, one voxel per thread), lp-ntPET vs MRTM."""
+    p = S.config2(J=40, N_per_model=3000, n=25, noise="mid", n_frames=100)
+    g, _ = run_gpu(p)
+    o, _ = run_oracle(p)
+    compare(g, o)
+
+
+@pytest.mark.parametrize("N", [12345, 40_000 + 77])
+def test_ragged_draw_counts(tb_small, N):
+    """N not a multiple of the tile / super-tile / hyper-tile sizes; fewer hyper-tiles than parts."""
+    half = N // 2
+    models = [dict(m, n_draws=(half if k == 0 else N - half)) for k, m in enumerate(tb_small.ctx_kwargs["models"])]
+    p = tb_small.replace(models=models).subset(np.arange(150))
+    g, _ = run_gpu(p)
+    o, _ = run_oracle(p)
+    compare(g, o)
+
+
+def test_l1_tb_and_eps_rt(tb_small, rt_small):
+    """L1 discrepancy on the TB shape; eps mode on the lp-ntPET / MRTM shape."""
+    p = tb_small.replace(distance="L1").subset(np.arange(200))
+    g, _ = run_gpu(p)
+    o, _ = run_oracle(p)
+    compare(g, o)
+    o_top, _ = run_oracle(rt_small)
+    eps = float(np.median(o_top["acc_dist"][:, -1]))
+    q = rt_small.replace(accept="EPS", epsilon=eps)
+    g, _ = run_gpu(q)
+    o, _ = run_oracle(q)
+    assert np.array_equal(g["count"], o["count"])
+    compare(g, o, topn=False)
+
+
 @pytest.mark.parametrize("J", [1, 31, 513, 1025])
 def test_ragged_voxel_counts(tb_small, J):
     idx = np.arange(J) % tb_small.J
