@@ -616,7 +616,17 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
     const uint64_t item = uint64_t(uint32_t(*s_item));
     __syncthreads();
     if (item >= nitems) break;
-    const uint64_t vt = item / S;
+#ifndef VPET_QORDER
+#define VPET_QORDER 1
+#endif
+    // queue order of voxel tiles: 1 = descending first-principal-axis projection (the voxel order
+    // is PC1-major Morton, reversed), i.e. high-activity voxels first: their thresholds are larger
+    // (noise grows with activity), so they are the long items and go first (longest-
+    // processing-time-first scheduling of the persistent queue).  0 = Morton order, 2 = strided.
+    const uint64_t nvt_ = nvt;
+    uint64_t vt = item / S;
+    if (VPET_QORDER == 1) vt = nvt_ - 1 - vt;
+    if (VPET_QORDER == 2) vt = (vt * 613ull) % nvt_;
     const uint32_t part = uint32_t(item % S);
     const uint64_t nsub = (p.nhyper > part) ? (p.nhyper - part + S - 1) / S : 0;  // hyper-tiles of this part
     Voxels<LP, R> V;
