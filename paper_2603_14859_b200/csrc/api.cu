@@ -81,7 +81,7 @@ struct abc_ctx {
   // work buffers
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
   DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, hbounds, tau_glob, queue;
-  DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp;
+  DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp, item_log;
   abc_stats stats{};
   bool bank_valid = false;
   uint64_t mem_sig[6] = {~0ull, 0, 0, 0, 0, 0};  // (J, N, flags, ptr_flags, n, L) of the last passed memory check
@@ -752,8 +752,25 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     sp.nparts = nparts;
     sp.bound_work = ctx->work.as<unsigned long long>() + 1;
     if (eps) CK(cudaMemsetAsync(ctx->mom.p, 0, sizeof(double) * J * M * MOMW, st));
+    // diagnostics: per-item timeline of the tree scan (env VPET_ITEMLOG=<file>)
+    const char* ilog = tree ? getenv("VPET_ITEMLOG") : nullptr;
+    const uint64_t nitems_dbg = ((J + 127) / 128) * nparts + 64;
+    if (ilog) {
+      CK(ctx->item_log.ensure(32 * nitems_dbg));
+      CK(cudaMemsetAsync(ctx->item_log.p, 0, 32 * nitems_dbg, st));
+      sp.item_log = ctx->item_log.as<unsigned long long>();
+    }
     CK(ctx->dist_wl2() ? launch_scan_wl2(sp, LP, count_work, tree, st) : launch_scan_l1(sp, LP, count_work, tree, st));
     ++launches;
+    if (ilog) {
+      std::vector<unsigned long long> hl(4 * nitems_dbg);
+      CK(cudaMemcpyAsync(hl.data(), ctx->item_log.p, 32 * nitems_dbg, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (FILE* fp = fopen(ilog, "wb")) {
+        fwrite(hl.data(), 8, hl.size(), fp);
+        fclose(fp);
+      }
+    }
   }
   rec(EV_SCAN);
 
@@ -901,7 +918,7 @@ void abc_destroy(abc_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs2[] = {&ctx->fmean, &ctx->cov, &ctx->pcs, &ctx->pminmax, &ctx->keys, &ctx->keys_alt, &ctx->vals,
                      &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob,
-                     &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp};
+                     &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp, &ctx->item_log};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,

@@ -266,6 +266,7 @@ struct ScanParams {
   uint32_t nparts;
   unsigned int* tau_glob;   // [J] float bits (positive), atomicMin
   unsigned int* queue;      // work-queue counter (zeroed per run)
+  unsigned long long* item_log;  // diagnostics (env VPET_ITEMLOG): [item][4] = start ns, end ns, SM, voxel tile
   const uint32_t* vorder;   // [J] voxel processed in slot j (tree mode) or nullptr (identity)
 };
 // Candidate heaps: 8-ary max-heaps; node i lives at slot i + kHeapOff of a (voxel, part) row of

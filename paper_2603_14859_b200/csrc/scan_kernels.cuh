@@ -617,17 +617,21 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
     __syncthreads();
     if (item >= nitems) break;
 #ifndef VPET_QORDER
-#define VPET_QORDER 1
+#define VPET_QORDER 3
 #endif
-    // queue order of voxel tiles: 1 = descending first-principal-axis projection (the voxel order
-    // is PC1-major Morton, reversed), i.e. high-activity voxels first: their thresholds are larger
-    // (noise grows with activity), so they are the long items and go first (longest-
-    // processing-time-first scheduling of the persistent queue).  0 = Morton order, 2 = strided.
+    // queue order of voxel tiles (the voxel order is PC1-major Morton): 3 = both ends of the PC1
+    // range first, alternating (0, last, 1, last-1, ...).  The extremes are the long items: high
+    // activity (thresholds grow with the noise) and near-zero TACs (where the prior puts
+    // many draws); longest-first scheduling of the persistent queue shortens the tail.
+    // 0 = Morton order, 1 = reversed, 2 = strided.
     const uint64_t nvt_ = nvt;
     uint64_t vt = item / S;
     if (VPET_QORDER == 1) vt = nvt_ - 1 - vt;
     if (VPET_QORDER == 2) vt = (vt * 613ull) % nvt_;
+    if (VPET_QORDER == 3) vt = (vt & 1) ? nvt_ - 1 - (vt >> 1) : (vt >> 1);  // both ends first
     const uint32_t part = uint32_t(item % S);
+    unsigned long long t_item0 = 0;
+    if (p.item_log && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item0));
     const uint64_t nsub = (p.nhyper > part) ? (p.nhyper - part + S - 1) / S : 0;  // hyper-tiles of this part
     Voxels<LP, R> V;
     load_voxels<LP, R>(p, V, tid, vt);
@@ -767,6 +771,17 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       }
     }
     store_counts<LP, R>(p, V, part);
+    if (p.item_log && tid == 0) {
+      unsigned long long t1, smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      smid = sm;
+      p.item_log[item * 4 + 0] = t_item0;
+      p.item_log[item * 4 + 1] = t1;
+      p.item_log[item * 4 + 2] = smid;
+      p.item_log[item * 4 + 3] = vt;
+    }
   }
   finish_counts(p, work, bwork, lane, COUNT);
 }

@@ -8,8 +8,7 @@ from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": (),
-    "qrev": ("VPET_QORDER=1",),
-    "qstride": ("VPET_QORDER=2",),
+    "qzig": ("VPET_QORDER=3",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
