@@ -239,17 +239,17 @@ __global__ void __launch_bounds__(256) proj_minmax_kernel(const OrderParams p) {
 #define VPET_BANKS 1.0f
 #endif
 #ifndef VPET_MBITS
-#define VPET_MBITS 15  // Morton bits per principal axis of the bank order
+#define VPET_MBITS 16  // Morton bits per principal axis of the bank order
 #endif
 constexpr int kMBits = VPET_MBITS;
 #ifndef VPET_BANK_MSB
 #define VPET_BANK_MSB 0
 #endif
 __device__ __forceinline__ unsigned long long spread4(unsigned long long x) {
-  // insert 3 zero bits between the low 15 bits of x (4-D Morton)
+  // insert 3 zero bits between the low 16 bits of x (4-D Morton)
   unsigned long long r = 0;
 #pragma unroll
-  for (int b = 0; b < 15; ++b) r |= ((x >> b) & 1ull) << (4 * b);
+  for (int b = 0; b < 16; ++b) r |= ((x >> b) & 1ull) << (4 * b);
   return r;
 }
 

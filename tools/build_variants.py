@@ -8,7 +8,7 @@ from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": (),
-    "qzig": ("VPET_QORDER=3",),
+    "mb16": ("VPET_MBITS=16",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
