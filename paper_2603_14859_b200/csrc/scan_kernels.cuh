@@ -24,6 +24,8 @@
 // re-scores them in FP64; eps mode re-scores every draw with D32 <= eps + err(eps) inline.
 #pragma once
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -56,6 +58,9 @@ constexpr int T = kTile;
 #ifndef VPET_RREFRESH
 #define VPET_RREFRESH 0  // and every VPET_RREFRESH rows inside a tile (0: off)
 #endif
+#ifndef VPET_SHEAP
+#define VPET_SHEAP 0  // keep the top of each candidate heap in shared memory (tree scan)
+#endif
 #ifndef VPET_SSORT
 #define VPET_SSORT 1
 #endif
@@ -71,9 +76,19 @@ struct Shape {
   static constexpr size_t STAGE_FLOATS = size_t(T) * LP;
   // prefetched boxes of one super-tile: its own [lo; hi] then its kSuper tiles' (double buffered)
   static constexpr size_t BOXB_FLOATS = size_t(kSuper + 1) * 2 * LP;
-  static constexpr size_t SMEM = size_t(NST) * (STAGE_FLOATS * 4 + T * 4) + NST * 8 + NST * 4 +
-                                 NW * 4 + NW * LP * 4 + 16 + 64 + size_t(kHyperSort) * (NW * 8 + 8 + NW * 4) + kHyperSort / 8 +
-                                 2 * BOXB_FLOATS * 4 + 16 + 16;
+  // the TMA ring; the best-first sort scratch aliases it (used only while the ring is idle)
+  static constexpr size_t RING_BYTES = size_t(NST) * STAGE_FLOATS * 4;
+  static constexpr size_t SCRATCH_BYTES = size_t(kHyperSort) * NW * 12 + kHyperSort / 8;
+#ifndef VPET_ALIAS
+#define VPET_ALIAS 1
+#endif
+  static constexpr size_t REGION = VPET_ALIAS ? ((RING_BYTES > SCRATCH_BYTES ? RING_BYTES : SCRATCH_BYTES) + 15) & ~size_t(15)
+                                              : ((RING_BYTES + SCRATCH_BYTES) + 15) & ~size_t(15);
+  // top of each voxel's candidate heap (root + its 8 children) kept in shared memory per item
+  static constexpr int KTOP = 9;
+  static constexpr size_t HTOP_BYTES = VPET_SHEAP ? size_t(NT) * R * KTOP * 8 : 0;
+  static constexpr size_t SMEM = REGION + size_t(NST) * T * 4 + NST * 8 + NST * 4 + NW * 4 + NW * LP * 4 + 16 + 64 +
+                                 size_t(kHyperSort) * 8 + 2 * BOXB_FLOATS * 4 + 16 + 16 + HTOP_BYTES + 16;
 
 };
 
@@ -145,6 +160,73 @@ static __device__ __noinline__ uint2 heap_push(unsigned long long* hb, uint32_t 
       pos = c0 + mj;
     }
     h[pos] = key;
+  }
+  return make_uint2(cnt, uint32_t(root >> 32));
+}
+
+// Same heap with nodes 0..8 (the root and its 8 children) in shared memory at byte address ts.
+__device__ __forceinline__ unsigned long long lds64(uint32_t a) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, unsigned long long v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+static __device__ __noinline__ uint2 heap_push_s(unsigned long long* hb, uint32_t ts, uint32_t K, uint32_t cnt,
+                                                 unsigned long long key) {
+  unsigned long long* h = hb + kHeapOff;
+  auto ld = [&](uint32_t i) { return i < 9 ? lds64(ts + 8 * i) : h[i]; };
+  auto st = [&](uint32_t i, unsigned long long v) {
+    if (i < 9) sts64(ts + 8 * i, v);
+    else h[i] = v;
+  };
+  unsigned long long root;
+  if (cnt < K) {
+    uint32_t pos = cnt++;
+    while (pos > 0) {
+      uint32_t par = (pos - 1) >> 3;
+      unsigned long long pk = ld(par);
+      if (pk >= key) break;
+      st(pos, pk);
+      pos = par;
+    }
+    st(pos, key);
+    if (cnt < K) return make_uint2(cnt, 0x7f800000u);
+    root = pos == 0 ? key : lds64(ts);
+  } else {
+    // level 1 (shared memory)
+    unsigned long long m = 0;
+    uint32_t mj = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) {
+      const unsigned long long c = lds64(ts + 8 * (1 + j));
+      if (1 + j < K && c > m) { m = c; mj = j; }
+    }
+    if (m <= key) {
+      sts64(ts, key);
+      root = key;
+    } else {
+      sts64(ts, m);
+      root = m;
+      uint32_t pos = 1 + mj;
+      for (;;) {  // levels >= 2 (global memory)
+        const uint32_t c0 = 8 * pos + 1;
+        if (c0 >= K) break;
+        const ulonglong2* g = reinterpret_cast<const ulonglong2*>(h + c0);
+        const ulonglong2 q0 = g[0], q1 = g[1], q2 = g[2], q3 = g[3];
+        const unsigned long long ch[8] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y, q3.x, q3.y};
+        unsigned long long mm = 0;
+        uint32_t mjj = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j)
+          if (c0 + j < K && ch[j] > mm) { mm = ch[j]; mjj = j; }
+        if (mm <= key) break;
+        st(pos, mm);
+        pos = c0 + mjj;
+      }
+      st(pos, key);
+    }
   }
   return make_uint2(cnt, uint32_t(root >> 32));
 }
@@ -312,9 +394,9 @@ struct Chunks {
 };
 
 // Evaluate one bank row (scan order) against the thread's voxels; insert survivors.
-template <int LP, int R, int DIST, bool COUNT>
+template <int LP, int R, int DIST, bool COUNT, bool SH = false>
 __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, const float* sr, uint64_t i,
-                                         uint32_t part, unsigned long long& work) {
+                                         uint32_t part, unsigned long long& work, uint32_t htop_s = 0) {
   float2 acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
@@ -337,7 +419,9 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
         if (!p.eps_mode) {
           unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
           if (COUNT && VPET_COUNT_PUSH) work += 1;
-          uint2 st = heap_push(p.heap + (uint64_t(V.vox[r]) * p.nparts + part) * heap_stride(p.K), p.K, V.cnt[r], key);
+          unsigned long long* hb = p.heap + (uint64_t(V.vox[r]) * p.nparts + part) * heap_stride(p.K);
+          uint2 st = SH ? heap_push_s(hb, htop_s + uint32_t(r) * NT * 72u, p.K, V.cnt[r], key)
+                        : heap_push(hb, p.K, V.cnt[r], key);
           V.cnt[r] = st.x;
           V.taup[r] = __uint_as_float(st.y);
           if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + V.vox[r], st.y);
@@ -384,10 +468,20 @@ __device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const float* b
 }
 
 template <int LP, int R>
-__device__ __forceinline__ void store_counts(const ScanParams& p, const Voxels<LP, R>& V, uint32_t part) {
+__device__ __forceinline__ void store_counts(const ScanParams& p, const Voxels<LP, R>& V, uint32_t part,
+                                             const unsigned long long* htop = nullptr) {
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    if (V.vox[r] < p.J && !p.eps_mode) p.heap_cnt[uint64_t(V.vox[r]) * p.nparts + part] = V.cnt[r];
+    if (V.vox[r] < p.J && !p.eps_mode) {
+      const uint64_t row = uint64_t(V.vox[r]) * p.nparts + part;
+      p.heap_cnt[row] = V.cnt[r];
+      if (htop) {  // write the shared-memory top of the heap back (certify reads the whole heap)
+        unsigned long long* h = p.heap + row * heap_stride(p.K) + kHeapOff;
+        const unsigned long long* t = htop + size_t(r) * NT * 9;
+        const uint32_t nt = V.cnt[r] < 9u ? V.cnt[r] : 9u;
+        for (uint32_t j = 0; j < nt; ++j) h[j] = t[j];
+      }
+    }
 }
 
 __device__ __forceinline__ void finish_counts(const ScanParams& p, unsigned long long work, unsigned long long bwork,
@@ -553,23 +647,30 @@ template <int LP, int DIST, bool COUNT>
 __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const ScanParams p) {
   constexpr int R = Shape<LP>::R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* stage = reinterpret_cast<float*>(smem_raw);
-  uint32_t* sidx = reinterpret_cast<uint32_t*>(smem_raw + NST * Shape<LP>::STAGE_FLOATS * 4);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NST * (Shape<LP>::STAGE_FLOATS * 4 + T * 4));
+  float* stage = reinterpret_cast<float*>(smem_raw);  // [NST][STAGE_FLOATS] TMA ring
+  // best-first sort scratch, aliasing the ring (the ring is idle whenever an order is computed)
+  unsigned long long* okeys = reinterpret_cast<unsigned long long*>(
+      smem_raw + (VPET_ALIAS ? 0 : Shape<LP>::RING_BYTES));  // [NW][kHyperSort]
+  float* hlb = reinterpret_cast<float*>(okeys + NW * kHyperSort);               // [NW][kHyperSort]
+  uint32_t* vis = reinterpret_cast<uint32_t*>(hlb + NW * kHyperSort);           // [kHyperSort / 32]
+  unsigned char* after = smem_raw + Shape<LP>::REGION;
+  uint32_t* sidx = reinterpret_cast<uint32_t*>(after);
+  uint64_t* full = reinterpret_cast<uint64_t*>(after + NST * T * 4);
   int* arrivals = reinterpret_cast<int*>(full + NST);
   uint32_t* wmask = reinterpret_cast<uint32_t*>(arrivals + NST);
   float* ybar = reinterpret_cast<float*>(wmask + NW);
   int* s_item = reinterpret_cast<int*>(ybar + NW * LP);
-  unsigned long long* okeys = reinterpret_cast<unsigned long long*>(
-      (reinterpret_cast<uintptr_t>(s_item + 4) + 15) & ~uintptr_t(15));  // [NW][kHyperSort] sort scratch
-  uint32_t* horder = reinterpret_cast<uint32_t*>(okeys + NW * kHyperSort);  // [kHyperSort] hyper-tile order
+  uint32_t* horder = reinterpret_cast<uint32_t*>(
+      (reinterpret_cast<uintptr_t>(s_item + 4) + 15) & ~uintptr_t(15));  // [kHyperSort] hyper-tile order
   uint32_t* sorder = horder + kHyperSort;                                  // [kHyperSort] super-tile order
-  uint32_t* vis = sorder + kHyperSort;                                     // [kHyperSort / 32]
-  float* hlb = reinterpret_cast<float*>(vis + kHyperSort / 32);            // [NW][kHyperSort]
   constexpr size_t BXF = Shape<LP>::BOXB_FLOATS;
   float* bbuf = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(hlb + NW * kHyperSort) + 15) & ~uintptr_t(15));  // [2][BXF]
+      (reinterpret_cast<uintptr_t>(sorder + kHyperSort) + 15) & ~uintptr_t(15));  // [2][BXF]
   uint64_t* bbar = reinterpret_cast<uint64_t*>(bbuf + 2 * BXF);                  // [2]
+  unsigned long long* htop = reinterpret_cast<unsigned long long*>(
+      (reinterpret_cast<uintptr_t>(bbar + 2) + 15) & ~uintptr_t(15));  // [R][NT][9] heap tops
+  unsigned long long* htop_t = VPET_SHEAP ? htop + threadIdx.x * 9 : nullptr;
+  const uint32_t htop_s = smem_u32(htop) + uint32_t(threadIdx.x) * 72u;  // this thread's heap tops (bytes)
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t N = p.N;
@@ -749,7 +850,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
           const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
           for (uint32_t d = 0; d < nd; ++d) {
             if (VPET_RREFRESH && d > 0 && (d % VPET_RREFRESH) == 0) refresh_tau<LP, R>(p, V);
-            eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, si[d], part, work);
+            eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, sb + d * LP, si[d], part, work, htop_s);
           }
         }
         __syncwarp();
@@ -770,7 +871,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       consumed += nal;
       }
     }
-    store_counts<LP, R>(p, V, part);
+    store_counts<LP, R>(p, V, part, htop_t);
     if (p.item_log && tid == 0) {
       unsigned long long t1, smid;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -804,6 +905,7 @@ cudaError_t launch_one(const ScanParams& p, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, S::SMEM);
+    if (getenv("VPET_SHOW_OCC")) fprintf(stderr, "scan LP=%d smem=%zu occupancy=%d CTAs/SM\n", LP, S::SMEM, occ);
     uint64_t slots = uint64_t(nsm) * uint64_t(occ > 0 ? occ : 1);
     uint64_t items = nvt * p.nparts;
     grid = items < slots ? items : slots;
