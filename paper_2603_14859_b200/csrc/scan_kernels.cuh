@@ -394,6 +394,40 @@ struct Chunks {
 };
 
 // Evaluate one bank row (scan order) against the thread's voxels; insert survivors.
+#ifndef VPET_COUNT_PUSH
+#define VPET_COUNT_PUSH 0  // tuning: count heap pushes instead of frame updates
+#endif
+#ifndef VPET_PUSHCHECK
+#define VPET_PUSHCHECK 0  // re-read the shared threshold before a heap push
+#endif
+// Insert the survivors of draw i (full D32 in acc) into the lanes' candidate heaps.
+template <int LP, int R, bool COUNT, bool SH>
+__device__ __forceinline__ void finish_row(const ScanParams& p, Voxels<LP, R>& V, const float2 (&acc)[R], uint64_t i,
+                                           uint32_t part, unsigned long long& work, uint32_t htop_s) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float D = __fadd_rn(acc[r].x, acc[r].y);
+    if (VPET_PUSHCHECK && D < V.tau[r] && !p.eps_mode && p.tau_glob)
+      V.tau[r] = fminf(V.tau[r], __uint_as_float(__ldcg(p.tau_glob + V.vox[r])));
+    if (D < V.tau[r]) {
+      if (!p.eps_mode) {
+        unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
+        if (COUNT && VPET_COUNT_PUSH) work += 1;
+        unsigned long long* hb = p.heap + (uint64_t(V.vox[r]) * p.nparts + part) * heap_stride(p.K);
+        uint2 st = SH ? heap_push_s(hb, htop_s + uint32_t(r) * NT * 72u, p.K, V.cnt[r], key)
+                      : heap_push(hb, p.K, V.cnt[r], key);
+        V.cnt[r] = st.x;
+        V.taup[r] = __uint_as_float(st.y);
+        if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + V.vox[r], st.y);
+        V.tau[r] = fminf(V.tau[r], V.taup[r]);
+      } else {
+        eps_candidate(p.tacs + uint64_t(V.vox[r]) * p.L, p.bank, p.LS, p.w, p.L, p.dist, p.eps,
+                      p.mom + uint64_t(V.vox[r]) * (size_t(p.M) * MOMW), p.prior_g, i);
+      }
+    }
+  }
+}
+
 template <int LP, int R, int DIST, bool COUNT, bool SH = false>
 __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, const float* sr, uint64_t i,
                                          uint32_t part, unsigned long long& work, uint32_t htop_s = 0) {
@@ -402,37 +436,40 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
   for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
   unsigned long long w = 0;
   bool go = Chunks<LP, R, DIST, false, 0>::run(V, sr, nullptr, acc, w, !p.prune);
-#ifndef VPET_COUNT_PUSH
-#define VPET_COUNT_PUSH 0  // tuning: count heap pushes instead of frame updates
-#endif
   if (COUNT && !VPET_COUNT_PUSH) work += w;
-  if (go) {
+  if (go) finish_row<LP, R, COUNT, SH>(p, V, acc, i, part, work, htop_s);
+}
+
+// Two rows at once: their first chunks run interleaved (twice the independent FMA chains, one
+// pair of votes), then each survivor continues alone.  Row B's first-chunk test may use the
+// threshold from before row A's inserts: a larger threshold only keeps more, so this is exact.
+template <int LP, int R, int DIST, bool COUNT, bool SH = false>
+__device__ __forceinline__ void eval_pair(const ScanParams& p, Voxels<LP, R>& V, const float* sa, uint64_t ia,
+                                          const float* sb, uint64_t ib, uint32_t part, unsigned long long& work,
+                                          uint32_t htop_s = 0) {
+  constexpr int NCH = (LP + CH - 1) / CH;
+  float2 aa[R], ab[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      float D = __fadd_rn(acc[r].x, acc[r].y);
-#ifndef VPET_PUSHCHECK
-#define VPET_PUSHCHECK 0  // re-read the shared threshold before a heap push
-#endif
-      if (VPET_PUSHCHECK && D < V.tau[r] && !p.eps_mode && p.tau_glob)
-        V.tau[r] = fminf(V.tau[r], __uint_as_float(__ldcg(p.tau_glob + V.vox[r])));
-      if (D < V.tau[r]) {
-        if (!p.eps_mode) {
-          unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
-          if (COUNT && VPET_COUNT_PUSH) work += 1;
-          unsigned long long* hb = p.heap + (uint64_t(V.vox[r]) * p.nparts + part) * heap_stride(p.K);
-          uint2 st = SH ? heap_push_s(hb, htop_s + uint32_t(r) * NT * 72u, p.K, V.cnt[r], key)
-                        : heap_push(hb, p.K, V.cnt[r], key);
-          V.cnt[r] = st.x;
-          V.taup[r] = __uint_as_float(st.y);
-          if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + V.vox[r], st.y);
-          V.tau[r] = fminf(V.tau[r], V.taup[r]);
-        } else {
-          eps_candidate(p.tacs + uint64_t(V.vox[r]) * p.L, p.bank, p.LS, p.w, p.L, p.dist, p.eps,
-                        p.mom + uint64_t(V.vox[r]) * (size_t(p.M) * MOMW), p.prior_g, i);
-        }
-      }
-    }
+  for (int r = 0; r < R; ++r) {
+    aa[r] = make_float2(0.0f, 0.0f);
+    ab[r] = make_float2(0.0f, 0.0f);
   }
+  dist_chunk<LP, R, DIST, 0>(V, sa, aa);
+  dist_chunk<LP, R, DIST, 0>(V, sb, ab);
+  unsigned long long w = 2ull * uint64_t((CH < LP ? CH : LP)) * R;
+  bool ga = any_alive<LP, R>(V, aa, !p.prune);
+  bool gb = any_alive<LP, R>(V, ab, !p.prune);
+  if constexpr (NCH > 1) {
+    if (ga) ga = Chunks<LP, R, DIST, false, 1>::run(V, sa, nullptr, aa, w, !p.prune);
+  }
+  if (COUNT && !VPET_COUNT_PUSH) work += w;
+  if (ga) finish_row<LP, R, COUNT, SH>(p, V, aa, ia, part, work, htop_s);
+  w = 0;
+  if constexpr (NCH > 1) {
+    if (gb) gb = Chunks<LP, R, DIST, false, 1>::run(V, sb, nullptr, ab, w, !p.prune);
+  }
+  if (COUNT && !VPET_COUNT_PUSH) work += w;
+  if (gb) finish_row<LP, R, COUNT, SH>(p, V, ab, ib, part, work, htop_s);
 }
 
 // Pull the other parts' progress on the shared thresholds.
@@ -848,10 +885,15 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
           const uint32_t* si = sidx + st * T;
           const uint64_t rem = N - t * T;
           const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
-          for (uint32_t d = 0; d < nd; ++d) {
-            if (VPET_RREFRESH && d > 0 && (d % VPET_RREFRESH) == 0) refresh_tau<LP, R>(p, V);
-            eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, sb + d * LP, si[d], part, work, htop_s);
-          }
+#ifndef VPET_PAIR
+#define VPET_PAIR 0
+#endif
+          uint32_t d = 0;
+          if (VPET_PAIR)
+            for (; d + 1 < nd; d += 2)
+              eval_pair<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, sb + d * LP, si[d], sb + (d + 1) * LP, si[d + 1],
+                                                              part, work, htop_s);
+          for (; d < nd; ++d) eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, sb + d * LP, si[d], part, work, htop_s);
         }
         __syncwarp();
         if (lane == 0) {

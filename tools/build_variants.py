@@ -8,8 +8,7 @@ from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": (),
-    "nosheap": ("VPET_SHEAP=0",),
-    "noalias_nosheap": ("VPET_ALIAS=0", "VPET_SHEAP=0"),
+    "nopair": ("VPET_PAIR=0",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
