@@ -88,6 +88,8 @@ struct abc_ctx {
   bool dist_wl2() const { return cfg.distance == ABC_DIST_WL2; }
   uint32_t bank_L = 0;
   cudaEvent_t ev[EV_N] = {};
+  cudaStream_t copy = nullptr;       // host->device TAC copies, overlapped with the bank / order stages
+  cudaEvent_t tacs_ready = nullptr;
   bool ev_ok = false;
 };
 
@@ -383,6 +385,12 @@ abc_status abc_init(const abc_config* cfg, abc_ctx** out) {
     return ABC_E_CUDA;
   }
   c->stream = c->own;
+  if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->tacs_ready, cudaEventDisableTiming) != cudaSuccess) {
+    cudaStreamDestroy(c->own);
+    delete c;
+    return ABC_E_CUDA;
+  }
   c->ev_ok = true;
   for (int k = 0; k < EV_N; ++k)
     if (cudaEventCreate(&c->ev[k]) != cudaSuccess) c->ev_ok = false;
@@ -634,15 +642,31 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   rec(EV_START);
   const float* d_tacs = tacs;
   if (host_tacs) {
-    CK(cudaMemcpyAsync(ctx->tacs.p, tacs, sizeof(float) * J * L, cudaMemcpyHostToDevice, st));
+    // the copy runs on its own stream, overlapped with the bank and bank-order stages (which do
+    // not read the TACs); the compute stream joins it before the first TAC reader.  ctx->tacs is
+    // free: the previous call ended with a stream synchronisation.
+    CK(cudaEventRecord(ctx->tacs_ready, st));
+    CK(cudaStreamWaitEvent(ctx->copy, ctx->tacs_ready, 0));
+    CK(cudaMemcpyAsync(ctx->tacs.p, tacs, sizeof(float) * J * L, cudaMemcpyHostToDevice, ctx->copy));
+    CK(cudaEventRecord(ctx->tacs_ready, ctx->copy));
     d_tacs = ctx->tacs.as<float>();
   }
   rec(EV_H2D);
   CK(cudaMemsetAsync(ctx->flag.p, 0, 16, st));
   CK(cudaMemsetAsync(ctx->fb_len.p, 0, 16, st));
   CK(cudaMemsetAsync(ctx->work.p, 0, 16, st));
-  finite_check_kernel<<<148, 256, 0, st>>>(d_tacs, J * L, ctx->flag.as<int>());
-  ++launches;
+  bool joined = false;
+  auto join_tacs = [&]() -> cudaError_t {  // before the first kernel that reads the TACs
+    if (joined) return cudaSuccess;
+    joined = true;
+    if (host_tacs) {
+      cudaError_t e = cudaStreamWaitEvent(st, ctx->tacs_ready, 0);
+      if (e != cudaSuccess) return e;
+    }
+    finite_check_kernel<<<148, 256, 0, st>>>(d_tacs, J * L, ctx->flag.as<int>());
+    ++launches;
+    return cudaGetLastError();
+  };
 
   // K1: bank
   BankParams bp{make_tables(ctx, LS), N, ctx->bank.as<float>()};
@@ -687,6 +711,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     }
     CK(launch_order(op, st, &launches));
     if (tree) {
+      CK(join_tacs());
       VoxelOrderParams vp{};
       vp.tacs = d_tacs;
       vp.J = J;
@@ -706,6 +731,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       CK(launch_voxel_order(vp, st, &launches));
     }
   }
+  CK(join_tacs());
   rec(EV_ORDER);
 
   if (!exact) {
@@ -929,6 +955,8 @@ void abc_destroy(abc_ctx* ctx) {
   for (int k = 0; k < EV_N; ++k)
     if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
   if (ctx->own) cudaStreamDestroy(ctx->own);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  if (ctx->tacs_ready) cudaEventDestroy(ctx->tacs_ready);
   delete ctx;
 }
 
