@@ -115,6 +115,26 @@ __device__ __forceinline__ void warp_sort_reg(double (&k)[E], uint32_t (&ix)[E],
   }
 }
 
+template <int E>
+__device__ void warp_sort_regs(double* key, uint32_t* idx, int lane) {
+  double k[E];
+  uint32_t ix[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    k[e] = key[e * 32 + lane];
+    ix[e] = idx ? idx[e * 32 + lane] : 0u;
+  }
+  __syncwarp();
+  if (idx) warp_sort_reg<E, true>(k, ix, lane);
+  else warp_sort_reg<E, false>(k, ix, lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    key[e * 32 + lane] = k[e];
+    if (idx) idx[e * 32 + lane] = ix[e];
+  }
+  __syncwarp();
+}
+
 // Sort n2 (power of two) smem keys (and indices if idx) ascending: registers for n2 <= 64.
 __device__ void warp_sort_any(double* key, uint32_t* idx, uint32_t n2, int lane) {
   if (n2 <= 32) {
@@ -132,22 +152,7 @@ __device__ void warp_sort_any(double* key, uint32_t* idx, uint32_t n2, int lane)
     }
     __syncwarp();
   } else if (n2 == 64) {
-    double k[2];
-    uint32_t ix[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      k[e] = key[e * 32 + lane];
-      ix[e] = idx ? idx[e * 32 + lane] : 0u;
-    }
-    __syncwarp();
-    if (idx) warp_sort_reg<2, true>(k, ix, lane);
-    else warp_sort_reg<2, false>(k, ix, lane);
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      key[e * 32 + lane] = k[e];
-      if (idx) idx[e * 32 + lane] = ix[e];
-    }
-    __syncwarp();
+    warp_sort_regs<2>(key, idx, lane);
   } else if (idx) {
     warp_sort_pairs(key, idx, n2, lane);
   } else {
@@ -204,6 +209,7 @@ __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* c
   const uint32_t c = cnt[pref];
   const bool tcm = kind <= ABC_2TCM_REV;
   const float NANF = __int_as_float(0x7fc00000);
+  // n <= 32: each lane draws the parameters of its accepted draw once, for all columns
   // n <= 32: each lane draws the parameters of its accepted draw once, for all columns
   const bool small = n <= 32;
   float thr[ABC_MAX_P];
