@@ -371,10 +371,13 @@ __global__ void __launch_bounds__(128) hyper_bounds_kernel(const OrderParams p, 
 // Voxel scan order.  VPET_VOXKEY = 1: first-principal-axis projection; D = 2 or 4: D-dimensional
 // Morton code of the projection on the first D principal axes, on the bank's isotropic grid.
 #ifndef VPET_VOXKEY
-#define VPET_VOXKEY 2
+#define VPET_VOXKEY 3
 #endif
 #ifndef VPET_VOXS
-#define VPET_VOXS 0.5f
+#define VPET_VOXS 0.25f
+#endif
+#ifndef VPET_VOXS3
+#define VPET_VOXS3 VPET_VOXS  // scale of the third and fourth axes
 #endif
 constexpr int kVoxDims = VPET_VOXKEY;
 constexpr int kVoxAxisBits = kVoxDims == 1 ? 32 : (kVoxDims == 2 ? 16 : (kVoxDims == 3 ? 20 : 15));
@@ -427,7 +430,7 @@ __global__ void __launch_bounds__(256) voxel_key_kernel(const VoxelOrderParams p
       const float top = float((1u << kVoxAxisBits) - 1u);
 #pragma unroll
       for (int c = 0; c < kVoxDims; ++c) {
-        const float sc = c == 0 ? sm_scale : sm_scale * VPET_VOXS;
+        const float sc = c == 0 ? sm_scale : (c == 1 ? sm_scale * VPET_VOXS : sm_scale * VPET_VOXS3);
         const float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sc, 0.0f), top);
         key |= spread_d((unsigned long long)q) << (kVoxDims - 1 - c);
       }
