@@ -10,7 +10,10 @@ namespace vpet {
 
 constexpr uint32_t kCtrTag = 0x56504554u;  // "VPET": 4th Philox counter word (R7)
 constexpr int kMaxLP = 128;
-constexpr int kNPC = 4;      // principal axes used for the draw order (order.cu)
+#ifndef VPET_NPC
+#define VPET_NPC 4
+#endif
+constexpr int kNPC = VPET_NPC;  // principal axes used for the draw order (order.cu)
 #ifndef VPET_TILE
 #define VPET_TILE 32
 #endif

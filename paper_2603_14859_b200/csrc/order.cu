@@ -241,7 +241,14 @@ __global__ void __launch_bounds__(256) proj_minmax_kernel(const OrderParams p) {
 #ifndef VPET_MBITS
 #define VPET_MBITS 16  // Morton bits per principal axis of the bank order
 #endif
-constexpr int kMBits = VPET_MBITS;
+constexpr int kMBits = (VPET_MBITS * kNPC <= 64) ? VPET_MBITS : 64 / kNPC;
+// insert kNPC - 1 zero bits between the low kMBits bits of x (kNPC-dimensional Morton)
+__device__ __forceinline__ unsigned long long spread_npc(unsigned long long x) {
+  unsigned long long r = 0;
+#pragma unroll
+  for (int b = 0; b < kMBits; ++b) r |= ((x >> b) & 1ull) << (kNPC * b);
+  return r;
+}
 #ifndef VPET_BANK_MSB
 #define VPET_BANK_MSB 0
 #endif
@@ -274,7 +281,7 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
     for (int c = 0; c < kNPC; ++c) {
       const float sc = c == 0 ? sm_scale : sm_scale * VPET_BANKS;
       float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sc, 0.0f), float((1u << kMBits) - 1u));
-      key |= spread4((unsigned long long)q) << (VPET_BANK_MSB ? kNPC - 1 - c : c);
+      key |= spread_npc((unsigned long long)q) << (VPET_BANK_MSB ? kNPC - 1 - c : c);
     }
     p.keys[i] = key;
     p.vals[i] = uint32_t(i);

@@ -7,12 +7,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
-    "v3s025": ("VPET_VOXKEY=3", "VPET_VOXS=0.25f"),
-    "v3s0125": ("VPET_VOXKEY=3", "VPET_VOXS=0.125f"),
-    "v3a": ("VPET_VOXKEY=3", "VPET_VOXS=0.35f", "VPET_VOXS3=0.12f"),
-    "v3b": ("VPET_VOXKEY=3", "VPET_VOXS=0.25f", "VPET_VOXS3=0.5f"),
-    "v4s025": ("VPET_VOXKEY=4", "VPET_VOXS=0.25f"),
-    "v4a": ("VPET_VOXKEY=4", "VPET_VOXS=0.35f", "VPET_VOXS3=0.12f"),
+    "base": (),
+    "npc3": ("VPET_NPC=3",),
+    "npc5": ("VPET_NPC=5",),
+    "npc6": ("VPET_NPC=6",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
