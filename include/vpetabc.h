@@ -89,6 +89,10 @@ typedef enum { ABC_INPUT_PWL = 0, ABC_INPUT_FENG = 1 } abc_input_kind;
 #define ABC_FLAG_NO_PRUNE 0x8u   /* FP32 pass evaluates all frames of every pair (A/B only) */
 #define ABC_FLAG_NO_REORDER 0x10u/* FP32 pass keeps the acquisition frame order (A/B only) */
 #define ABC_FLAG_NO_TREE 0x20u   /* FP32 pass scans every draw in index order, no bounds (A/B only) */
+#define ABC_FLAG_DENSE_TC 0x40u  /* replace the FP32 pass by the dense shared-bank tensor-core
+                                    distance (y.s cross term on tcgen05, BF16x3 split; WL2, TOPN,
+                                    L <= 48, else ABC_E_UNSUPPORTED).  Same certified results;
+                                    evaluates every pair (SURVEY.md §8f-1, A/B comparison) */
 
 /* abc_run_voxels ptr_flags */
 #define ABC_PTR_TACS_DEVICE 0x1u /* tacs is a device pointer on ctx's device */

@@ -82,6 +82,7 @@ struct abc_ctx {
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
   DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, hbounds, tau_glob, queue;
   DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp, item_log;
+  DevBuf dBt, dS2, dAt, dY2;  // ABC_FLAG_DENSE_TC operands (dense_tc.cu)
   abc_stats stats{};
   bool bank_valid = false;
   uint64_t mem_sig[6] = {~0ull, 0, 0, 0, 0, 0};  // (J, N, flags, ptr_flags, n, L) of the last passed memory check
@@ -293,6 +294,26 @@ ErrBound error_bound(const abc_ctx* c, uint32_t LP) {
   return e;
 }
 
+// Rigorous |D' - D| bound of the dense dot form (ABC_FLAG_DENSE_TC, dense_tc.cu),
+// doubled for margin.  With a = fl(ws y), b = fl(ws s), Z = sum w (|y| + |s|)^2 <= 4 Y2 + 4 sqrt(Y2 D) + D:
+//   prescaling        |sum (a-b)^2 - D| <= (2u + u^2) D + 2u sqrt(D Z) + u^2 Z
+//   Y2, S2 in FP32    gamma_{L+1} (sum a^2 + sum b^2)
+//   G on tcgen05      (3.01 * 2^-18 [dropped split terms] + 144 * 2^-23 [FP32 accumulation, any
+//                     order, truncating adds]) sum |a b|
+//   final fadd, ffma  u (Y2 + S2) + u |D'|
+// all <= C Z + 2u D + 2u sqrt(D Z), C = gamma_{L+1} + 2u + c_G (+ u^2 terms absorbed).
+ErrBound dense_error_bound(uint32_t L) {
+  const double u = std::ldexp(1.0, -24);
+  const double g = (L + 1) * u / (1.0 - (L + 1) * u);
+  const double cG = 3.01 * std::ldexp(1.0, -18) + 144.0 * std::ldexp(1.0, -23);
+  const double C = g + 2.0 * u + cG + 4.0 * u * u;
+  ErrBound e{0, 0, 0, 0};
+  e.a = 2.0 * (C + 4.0 * u);
+  e.b = 2.0 * (4.0 * C + 4.0 * u);
+  e.c = 2.0 * 4.0 * C;
+  return e;
+}
+
 }  // namespace
 
 namespace vpet {
@@ -501,6 +522,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const bool exact = (ctx->cfg.flags & ABC_FLAG_EXACT) && !eps;
   const bool timing = (ctx->cfg.flags & ABC_FLAG_TIMING) && ctx->ev_ok;
   const bool count_work = (ctx->cfg.flags & ABC_FLAG_COUNT_WORK) != 0;
+  const bool dense = (ctx->cfg.flags & ABC_FLAG_DENSE_TC) && !exact;
+  if (dense && (eps || !ctx->dist_wl2() || L > 48))
+    return fail(ctx, ABC_E_UNSUPPORTED, "ABC_FLAG_DENSE_TC needs WL2, top-n acceptance and L <= 48");
   const uint32_t n = ctx->cfg.n_accept;
   uint32_t K = 0;
   if (!eps) {
@@ -528,8 +552,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     if (d.user && host_out) out_bytes += (d.bytes + 255) & ~size_t(255);
   size_t need = 0;
   need += sizeof(float) * N * LS;                        // exact bank
-  if (!exact) need += sizeof(float) * N * LP;            // scan bank
-  const bool tree = !exact && !(ctx->cfg.flags & ABC_FLAG_NO_TREE) && N < (1ull << 31);
+  if (!exact && !dense) need += sizeof(float) * N * LP;  // scan bank
+  if (dense) need += dense_bank_bytes(N) + dense_voxel_bytes(J) + 4 * J;
+  const bool tree = !exact && !dense && !(ctx->cfg.flags & ABC_FLAG_NO_TREE) && N < (1ull << 31);
   const uint64_t ntile = (N + kTile - 1) / kTile, nsuper = (ntile + kSuper - 1) / kSuper;
   const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
   // draw-range split of the tree scan (interleaved super-tiles): balances heavy voxels over SMs
@@ -548,6 +573,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const uint64_t nhyper = (nsuper + hs - 1) / hs;
   if (nparts > nhyper) nparts = uint32_t(nhyper);
   if (nparts == 0) nparts = 1;
+  if (dense) nparts = 2;  // the two column halves of each draw tile (dense_tc.cu)
   const size_t vsort_tmp = tree ? voxel_sort_temp_bytes(J) : 0;
   if (tree) need += N * (8 + 8 + 4 + 4 + 4) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper + nhyper);
   if (tree) need += 24 * J + vsort_tmp;
@@ -567,7 +593,15 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   }
 
   CK(ctx->bank.ensure(sizeof(float) * N * LS));
-  if (!exact) CK(ctx->bankp.ensure(sizeof(float) * N * LP));
+  if (!exact && !dense) CK(ctx->bankp.ensure(sizeof(float) * N * LP));
+  if (dense) {
+    const uint64_t Npad = (N + 255) / 256 * 256, Jpad = (J + 127) / 128 * 128;
+    CK(ctx->dBt.ensure(Npad * 144 * 2));
+    CK(ctx->dS2.ensure(Npad * 4));
+    CK(ctx->dAt.ensure(Jpad * 144 * 2));
+    CK(ctx->dY2.ensure(Jpad * 4));
+    CK(ctx->tau_glob.ensure(4 * J));
+  }
   CK(ctx->var.ensure(sizeof(double) * kMaxLP));
   CK(ctx->fmean.ensure(sizeof(double) * kMaxLP));
   if (tree) {
@@ -676,8 +710,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   ctx->bank_L = L;
   rec(EV_BANK);
 
-  const ErrBound eb = error_bound(ctx, LP);
-  if (!exact) {
+  const ErrBound eb = dense ? dense_error_bound(L) : error_bound(ctx, LP);
+  if (!exact && !dense) {
     OrderParams op{};
     op.bank = ctx->bank.as<float>();
     op.N = N;
@@ -734,7 +768,23 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   CK(join_tacs());
   rec(EV_ORDER);
 
-  if (!exact) {
+  if (dense) {
+    DenseParams dp{};
+    dp.Bt = ctx->dBt.as<uint16_t>();
+    dp.S2 = ctx->dS2.as<float>();
+    dp.At = ctx->dAt.as<uint16_t>();
+    dp.Y2 = ctx->dY2.as<float>();
+    dp.N = N;
+    dp.J = J;
+    dp.L = L;
+    dp.K = K;
+    dp.heap = ctx->heap.as<unsigned long long>();
+    dp.heap_cnt = ctx->heap_cnt.as<uint32_t>();
+    dp.tau_glob = ctx->tau_glob.as<unsigned int>();
+    launch_fill_u32(ctx->tau_glob.as<uint32_t>(), 0x7f800000u, J, st);
+    ++launches;
+    CK(launch_dense(dp, ctx->bank.as<float>(), LS, d_tacs, ctx->d_wsc.as<float>(), st, &launches));
+  } else if (!exact) {
     ScanParams sp{};
     sp.bankp = ctx->bankp.as<float>();
     sp.N = N;
@@ -802,8 +852,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
 
   ReduceParams rp{};
   rp.K = K;
-  rp.nparts = (tree && !eps) ? nparts : 1;
-  rp.tau_glob = (tree && !eps) ? ctx->tau_glob.as<unsigned int>() : nullptr;
+  rp.nparts = ((tree || dense) && !eps) ? nparts : 1;
+  rp.tau_glob = ((tree || dense) && !eps) ? ctx->tau_glob.as<unsigned int>() : nullptr;
   rp.heap = ctx->heap.as<unsigned long long>();
   rp.heap_cnt = ctx->heap_cnt.as<uint32_t>();
   rp.hd = ctx->hd.as<double>();
@@ -944,7 +994,8 @@ void abc_destroy(abc_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs2[] = {&ctx->fmean, &ctx->cov, &ctx->pcs, &ctx->pminmax, &ctx->keys, &ctx->keys_alt, &ctx->vals,
                      &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob,
-                     &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp, &ctx->item_log};
+                     &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp, &ctx->item_log,
+                     &ctx->dBt, &ctx->dS2, &ctx->dAt, &ctx->dY2};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,

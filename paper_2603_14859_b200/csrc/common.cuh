@@ -347,4 +347,22 @@ void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st);
 
 void launch_fill_u32(uint32_t* p, uint32_t v, uint64_t n, cudaStream_t st);
 
+// K6 (dense_tc.cu): shared-bank tensor-core distance, ABC_FLAG_DENSE_TC (WL2, top-n, L <= 48).
+// Operands live in HBM pre-tiled in the UMMA no-swizzle K-major core-matrix layout (bf16 bits).
+struct DenseParams {
+  uint16_t* Bt;             // [Npad/256][256 x 144] bank operand [b_hi | b_lo | b_hi]
+  float* S2;                // [Npad] sum b^2 (FP32; +inf for padding rows)
+  uint16_t* At;             // [Jpad/128][128 x 144] voxel operand [a_hi | a_hi | a_lo]
+  float* Y2;                // [Jpad] sum a^2 (FP32)
+  uint64_t N, J, ntile;
+  uint32_t L, K;
+  unsigned long long* heap;  // [J][2][heap_stride(K)]: part = column half of each draw tile
+  uint32_t* heap_cnt;        // [J][2]
+  unsigned int* tau_glob;    // [J]
+};
+uint64_t dense_bank_bytes(uint64_t N);
+uint64_t dense_voxel_bytes(uint64_t J);
+cudaError_t launch_dense(DenseParams p, const float* bank, uint32_t LS, const float* tacs, const float* wsc,
+                         cudaStream_t st, uint32_t* launches);
+
 }  // namespace vpet
