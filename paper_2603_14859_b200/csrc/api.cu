@@ -528,7 +528,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const uint32_t n = ctx->cfg.n_accept;
   uint32_t K = 0;
   if (!eps) {
-    uint64_t k = uint64_t(n) + std::max<uint64_t>(8, n / 16);
+    // dense mode: a wider candidate band, since its dot-form error bound is ~1e-4 of ||y||^2 (vs ~u D)
+    uint64_t k = dense ? 4 * uint64_t(n) + 64 : uint64_t(n) + std::max<uint64_t>(8, n / 16);
     k = (k + 7) & ~7ull;
     K = uint32_t(std::min<uint64_t>(k, N));
   }

@@ -35,7 +35,8 @@ constexpr int BN = 256;         // draws per tile
 constexpr int NTH = 256;        // 8 warps: warp w reads TMEM lanes 32 (w % 4) .., column half w / 4
 constexpr uint32_t A_BYTES = BM * KD * 2;
 constexpr uint32_t B_BYTES = BN * KD * 2;
-constexpr uint32_t SMEM = A_BYTES + 2 * B_BYTES + 64;
+constexpr uint32_t CAND_BYTES = 8 * NTH * 8;  // 8 candidate slots per thread ([slot][thread])
+constexpr uint32_t SMEM = A_BYTES + 2 * B_BYTES + CAND_BYTES + 64;
 constexpr uint32_t TMEM_COLS = 512;
 
 // element offset of (row, k) in a tile of R rows: core matrix (row / 8, k / 8), K-chunk-major
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(NTH, 1) dense_tc_kernel(const DenseParams p) {
   uint64_t* full = bars + 1;
   uint64_t* done = bars + 3;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 5);
+  unsigned long long* sbuf = reinterpret_cast<unsigned long long*>(smem + A_BYTES + 2 * B_BYTES + 64);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int q = wid & 3, half = wid >> 2;
@@ -229,26 +231,51 @@ __global__ void __launch_bounds__(NTH, 1) dense_tc_kernel(const DenseParams p) {
 #pragma unroll 1
       for (int c = 0; c < BN / 2 / 32; ++c) {
         uint32_t g[32];
-        __syncwarp();  // tcgen05.ld is warp-collective: reconverge after the divergent heap pushes
+        __syncwarp();  // tcgen05.ld is warp-collective: reconverge after the heap pushes
         tmem_ld32(tbase + (uint32_t(q * 32) << 16) + uint32_t(s) * BN + uint32_t(half) * (BN / 2) + uint32_t(c) * 32u,
                   g);
         const float4* s2p = reinterpret_cast<const float4*>(p.S2 + i0 + uint64_t(c) * 32);
+        float4 s4[8];
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) s4[j4] = __ldg(s2p + j4);
+        // D' = fl(fl(Y2 + S2) - 2 G) (clamped at 0 below), in place of G
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 s4 = __ldg(s2p + j4);
-          const float s2v[4] = {s4.x, s4.y, s4.z, s4.w};
+          const float s2v[4] = {s4[j4].x, s4[j4].y, s4[j4].z, s4[j4].w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = j4 * 4 + e;
-            const float D = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(g[j]), __fadd_rn(y2, s2v[e])), 0.0f);
+          for (int e = 0; e < 4; ++e)
+            g[j4 * 4 + e] = __float_as_uint(__fmaf_rn(-2.0f, __uint_as_float(g[j4 * 4 + e]), __fadd_rn(y2, s2v[e])));
+        }
+        // fast path: one vote per 8 columns on the minimum; most groups hold no candidate
+#pragma unroll
+        for (int grp = 0; grp < 4; ++grp) {
+          float m = __uint_as_float(g[grp * 8]);
+#pragma unroll
+          for (int e = 1; e < 8; ++e) m = fminf(m, __uint_as_float(g[grp * 8 + e]));
+          if (!__any_sync(0xffffffffu, fmaxf(m, 0.0f) < tau)) continue;
+          // slow path: compact this lane's candidates into its shared-memory slots, then push them
+          // with the warp in lockstep (rounds = the largest per-lane count, not the sum)
+          uint32_t nb = 0;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float D = fmaxf(__uint_as_float(g[grp * 8 + e]), 0.0f);
             if (D < tau) {
-              const uint64_t i = i0 + uint64_t(c) * 32 + uint64_t(j);
-              const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
-              const uint2 st = scan::heap_push(hb, p.K, cnt, key);
-              cnt = st.x;
-              taup = __uint_as_float(st.y);
-              if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + v, st.y);
-              tau = fminf(tau, taup);
+              const uint32_t i = uint32_t(i0 + uint64_t(c) * 32 + uint64_t(grp * 8 + e));
+              sbuf[nb * NTH + tid] = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | i;
+              ++nb;
+            }
+          }
+          const uint32_t rounds = __reduce_max_sync(0xffffffffu, nb);
+          for (uint32_t k = 0; k < rounds; ++k) {
+            if (k < nb) {
+              const unsigned long long key = sbuf[k * NTH + tid];
+              if (__uint_as_float(uint32_t(key >> 32)) < tau) {
+                const uint2 st = scan::heap_push(hb, p.K, cnt, key);
+                cnt = st.x;
+                taup = __uint_as_float(st.y);
+                if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + v, st.y);
+                tau = fminf(tau, taup);
+              }
             }
           }
         }

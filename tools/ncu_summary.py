@@ -22,6 +22,12 @@ WANT = [
     "sm__maximum_warps_per_active_cycle_pct", "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
     "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__cycles_elapsed.avg.per_second",
     "l1tex__t_bytes.sum", "smsp__sass_thread_inst_executed_op_fadd_pred_on.sum",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
     "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", "launch__shared_mem_per_block_dynamic",
 ]
 

@@ -41,7 +41,7 @@ for N in [int(x) for x in a.draws.split(",")]:
             ctx = AbcContext(**dict(prob.ctx_kwargs, flags=flags))
             prob.setup(ctx)
             sts, res = [], None
-            for _ in range(a.reps + 1):
+            for _ in range(max(1, a.reps) + 1):
                 res = ctx.run_voxels(prob.tacs, want=("acc_idx", "prob"))
                 sts.append(ctx.stats())
             sts = sts[1:]
