@@ -60,6 +60,7 @@ def lib():
         L.abc_set_frames.argtypes = [vp, vp, vp, vp, C.c_uint32]
         L.abc_run_voxels.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.POINTER(Result)]
         L.abc_model_select.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp]
+        L.abc_response_envelope.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, C.c_uint32, C.c_uint32, vp]
         L.abc_last_error.argtypes = [vp]
         L.abc_last_error.restype = C.c_char_p
         L.abc_destroy.argtypes = [vp]
@@ -217,6 +218,15 @@ class OracleContext:
         th[: len(theta)] = np.asarray(theta, dtype=np.float32)
         out = np.zeros(self.L, dtype=np.float64)
         self._check(lib().oracle_simulate(self._h, KINDS[kind], _ptr(th), _ptr(out)))
+        return out
+
+    def response_envelope(self, acc_idx, t):
+        """J x T x 3 (2.5/50/97.5 %) of 1 + gamma/k2a g(t) over accepted lp-ntPET draws."""
+        idx = np.ascontiguousarray(acc_idx, dtype=np.uint64)
+        tt = np.ascontiguousarray(t, dtype=np.float64)
+        J, n = idx.shape
+        out = np.zeros((J, tt.size, 3), dtype=np.float32)
+        self._check(lib().abc_response_envelope(self._h, _ptr(idx), J, n, _ptr(tt), tt.size, 0, _ptr(out)))
         return out
 
     def bank(self):

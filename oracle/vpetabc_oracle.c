@@ -752,6 +752,65 @@ abc_status abc_model_select(abc_ctx* c, const float* tacs, uint64_t J, uint32_t 
   return abc_run_voxels(c, tacs, J, ptr_flags, &r);
 }
 
+/* Response-function credible envelope (Fig. 1).  For voxel j and time t_k: the
+ * type-7 2.5/50/97.5 % quantiles, over the voxel's accepted lp-ntPET draws, of
+ *   r(t) = k2a(t)/k2a = 1 + (gamma/k2a) g(t; tD, tP, alpha)          (eq:Bt P:90-94)
+ * with g the peak-normalised gamma variate above (R4).  Draws of other models are
+ * skipped (the envelope is that of "the lp-ntPET model", Fig. 1; R16); NaN when a voxel
+ * has none.  acc_idx: J x n_acc (host); q: J x T x 3 (host).  Plain loops, FP64, qsort. */
+abc_status abc_response_envelope(abc_ctx* c, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc,
+                                 const double* t, uint32_t T, uint32_t ptr_flags, float* q) {
+  if (!c) return ABC_E_ARG;
+  if (ptr_flags != 0) return fail(c, ABC_E_ARG, "the oracle takes host pointers only");
+  if (J == 0) return ABC_OK;
+  if (!acc_idx || !t || !q || n_acc == 0 || T == 0 || T > 1024) return fail(c, ABC_E_ARG, "bad envelope arguments");
+  int has_lp = 0;
+  for (uint32_t m = 0; m < c->cfg.n_models; ++m) has_lp |= c->cfg.model[m].kind == ABC_LPNTPET;
+  if (!has_lp) return fail(c, ABC_E_UNSUPPORTED, "no lp-ntPET model in the context");
+  for (uint32_t k = 0; k < T; ++k)
+    if (!isfinite(t[k])) return fail(c, ABC_E_ARG, "non-finite time");
+  const uint64_t N = total_draws(&c->cfg);
+  for (uint64_t e = 0; e < J * n_acc; ++e)
+    if (acc_idx[e] >= N) return fail(c, ABC_E_ARG, "draw index out of range");
+  double* v = (double*)malloc(sizeof(double) * n_acc);
+  float(*th)[ABC_MAX_P] = malloc(sizeof(float) * ABC_MAX_P * n_acc);
+  if (!v || !th) {
+    free(v);
+    free(th);
+    return fail(c, ABC_E_NOMEM, "envelope buffers");
+  }
+  for (uint64_t j = 0; j < J; ++j) {
+    uint32_t cnt = 0;
+    for (uint32_t a = 0; a < n_acc; ++a) {
+      int32_t m;
+      float x[ABC_MAX_P];
+      draw_theta(&c->cfg, acc_idx[j * n_acc + a], &m, x);
+      if (c->cfg.model[m].kind != ABC_LPNTPET) continue;
+      for (uint32_t k = 0; k < ABC_MAX_P; ++k) th[cnt][k] = x[k];
+      ++cnt;
+    }
+    for (uint32_t k = 0; k < T; ++k) {
+      float* o = q + (j * T + k) * 3;
+      if (cnt == 0) {
+        o[0] = o[1] = o[2] = NAN;
+        continue;
+      }
+      for (uint32_t a = 0; a < cnt; ++a) {
+        /* columns: R1, k2, k2a, gamma, tD, tP, alpha */
+        double ratio = (double)th[a][3] / (double)th[a][2];
+        v[a] = 1.0 + ratio * oracle_gamma_variate(th[a][4], th[a][5], th[a][6], t[k]);
+      }
+      qsort(v, cnt, sizeof(double), cmp_dbl);
+      o[0] = (float)oracle_quantile7(v, cnt, 0.025);
+      o[1] = (float)oracle_quantile7(v, cnt, 0.5);
+      o[2] = (float)oracle_quantile7(v, cnt, 0.975);
+    }
+  }
+  free(v);
+  free(th);
+  return ABC_OK;
+}
+
 const char* abc_last_error(const abc_ctx* c) { return c ? c->err : "null context"; }
 
 void abc_destroy(abc_ctx* c) {

@@ -87,6 +87,10 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
                           abc_result* out);
 abc_status abc_model_select(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t ptr_flags,
                             float* prob, int32_t* preferred);
+/* Response-function 95 % CrI envelope (Fig. 1): J x T x 3 quantiles of
+ * 1 + gamma/k2a g(t) over each voxel's accepted lp-ntPET draws (host pointers only). */
+abc_status abc_response_envelope(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc,
+                                 const double* t_min, uint32_t T, uint32_t ptr_flags, float* q);
 const char* abc_last_error(const abc_ctx* ctx);
 void abc_destroy(abc_ctx* ctx);
 
