@@ -203,6 +203,20 @@ abc_status abc_get_stats(const abc_ctx* ctx, abc_stats* stats);
  * ABC_E_STATE before the first run; ABC_E_ARG if the rows are out of range. */
 abc_status abc_get_bank(const abc_ctx* ctx, float* out, uint64_t first, uint64_t count);
 
+/* Response-function 95 % credible envelope (Fig. 1).  For voxel j
+ * and time t_min[k]: the type-7 2.5/50/97.5 % quantiles, over the voxel's accepted draws of an
+ * lp-ntPET model, of the response function
+ *     r(t) = k2a(t)/k2a = 1 + (gamma/k2a) g(t; tD, tP, alpha)      (eq:Bt P:90-94)
+ * with g the peak-normalised gamma variate (R4), in FP64 from the FP32 draws.  Draws of
+ * other models are skipped (R16); a voxel without lp-ntPET draws gets NaN.
+ * acc_idx: J x n_acc draw indices (e.g. abc_result.acc_idx of a TOPN run); host, or device if
+ * ptr_flags has ABC_PTR_TACS_DEVICE.  t_min: T times (host, finite).  q: J x T x 3 FP32,
+ * caller-allocated; host, or device if ptr_flags has ABC_PTR_OUT_DEVICE.  1 <= n_acc <= 4096,
+ * 1 <= T <= 1024, else ABC_E_ARG; ABC_E_ARG also for an index >= N (detected on device, after
+ * the work).  ABC_E_UNSUPPORTED if ctx has no lp-ntPET model.  Blocks until q is complete. */
+abc_status abc_response_envelope(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc,
+                                 const double* t_min, uint32_t T, uint32_t ptr_flags, float* q);
+
 const char* abc_last_error(const abc_ctx* ctx);
 void abc_destroy(abc_ctx* ctx);
 uint32_t abc_abi_version(void);

@@ -154,3 +154,25 @@ class AbcContext:
 
     def model_select(self, tacs):
         return self.run_voxels(tacs, want=("prob", "preferred"))
+
+    def response_envelope(self, acc_idx, t):
+        """J x T x 3 (2.5/50/97.5 %) quantiles of 1 + gamma/k2a g(t) over each voxel's accepted
+        lp-ntPET draws (Fig. 1).  acc_idx: J x n uint64 (numpy, or a torch CUDA tensor:
+        the result is then a torch CUDA tensor); t: times in minutes."""
+        tt = np.ascontiguousarray(t, dtype=np.float64)
+        T = int(tt.size)
+        if type(acc_idx).__module__.startswith("torch") and acc_idx.is_cuda:
+            import torch
+            idx = acc_idx.to(torch.int64).contiguous()
+            J, n = int(idx.shape[0]), int(idx.shape[1])
+            out = torch.empty((J, T, 3), dtype=torch.float32, device=idx.device)
+            self._check(self._lib.abc_response_envelope(self._h, C.c_void_p(idx.data_ptr()), J, n, tt.ctypes.data, T,
+                                                        A.PTR_TACS_DEVICE | A.PTR_OUT_DEVICE,
+                                                        C.c_void_p(out.data_ptr())))
+            return out
+        idx = np.ascontiguousarray(acc_idx, dtype=np.uint64)
+        J, n = idx.shape
+        out = np.zeros((J, T, 3), dtype=np.float32)
+        self._check(self._lib.abc_response_envelope(self._h, idx.ctypes.data, J, n, tt.ctypes.data, T, 0,
+                                                    out.ctypes.data))
+        return out

@@ -83,6 +83,7 @@ struct abc_ctx {
   DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, hbounds, tau_glob, queue;
   DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp, item_log;
   DevBuf dBt, dS2, dAt, dY2;  // ABC_FLAG_DENSE_TC operands (dense_tc.cu)
+  DevBuf env_idx, env_t, env_q;  // abc_response_envelope staging
   abc_stats stats{};
   bool bank_valid = false;
   uint64_t mem_sig[6] = {~0ull, 0, 0, 0, 0, 0};  // (J, N, flags, ptr_flags, n, L) of the last passed memory check
@@ -975,6 +976,47 @@ abc_status abc_model_select(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_
   return abc_run_voxels(ctx, tacs, J, ptr_flags, &r);
 }
 
+abc_status abc_response_envelope(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc,
+                                 const double* t_min, uint32_t T, uint32_t ptr_flags, float* q) {
+  if (!ctx) return ABC_E_ARG;
+  if (ptr_flags & ~(ABC_PTR_TACS_DEVICE | ABC_PTR_OUT_DEVICE)) return fail(ctx, ABC_E_ARG, "unknown ptr_flags");
+  if (J == 0) return ABC_OK;
+  if (!acc_idx || !t_min || !q || n_acc == 0 || n_acc > 4096 || T == 0 || T > 1024)
+    return fail(ctx, ABC_E_ARG, "bad envelope arguments");
+  bool has_lp = false;
+  for (uint32_t m = 0; m < ctx->M; ++m) has_lp |= ctx->prior.m[m].kind == ABC_LPNTPET;
+  if (!has_lp) return fail(ctx, ABC_E_UNSUPPORTED, "no lp-ntPET model in the context");
+  for (uint32_t k = 0; k < T; ++k)
+    if (!std::isfinite(t_min[k])) return fail(ctx, ABC_E_ARG, "non-finite time");
+  CK(cudaSetDevice(ctx->dev));
+  const cudaStream_t st = ctx->stream;
+  const bool dev_idx = ptr_flags & ABC_PTR_TACS_DEVICE, dev_out = ptr_flags & ABC_PTR_OUT_DEVICE;
+  const uint64_t* d_idx = acc_idx;
+  if (!dev_idx) {
+    CK(ctx->env_idx.ensure(8 * J * n_acc));
+    CK(cudaMemcpyAsync(ctx->env_idx.p, acc_idx, 8 * J * n_acc, cudaMemcpyHostToDevice, st));
+    d_idx = ctx->env_idx.as<uint64_t>();
+  }
+  CK(ctx->env_t.ensure(8 * T));
+  CK(cudaMemcpyAsync(ctx->env_t.p, t_min, 8 * T, cudaMemcpyHostToDevice, st));
+  float* d_q = q;
+  if (!dev_out) {
+    CK(ctx->env_q.ensure(12 * J * T));
+    d_q = ctx->env_q.as<float>();
+  }
+  CK(ctx->flag.ensure(16));
+  CK(cudaMemsetAsync(ctx->flag.p, 0, 16, st));
+  EnvelopeParams ep{d_idx, J, ctx->N, n_acc, T, ctx->env_t.as<double>(), ctx->prior, d_q, ctx->flag.as<int>()};
+  launch_response_envelope(ep, st);
+  CK(cudaGetLastError());
+  if (!dev_out) CK(cudaMemcpyAsync(q, d_q, 12 * J * T, cudaMemcpyDeviceToHost, st));
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, ctx->flag.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (bad) return fail(ctx, ABC_E_ARG, "draw index out of range");
+  return ABC_OK;
+}
+
 abc_status abc_get_bank(const abc_ctx* ctx_c, float* out, uint64_t first, uint64_t count) {
   abc_ctx* ctx = const_cast<abc_ctx*>(ctx_c);
   if (!ctx || !out) return ABC_E_ARG;
@@ -996,7 +1038,8 @@ void abc_destroy(abc_ctx* ctx) {
   DevBuf* bufs2[] = {&ctx->fmean, &ctx->cov, &ctx->pcs, &ctx->pminmax, &ctx->keys, &ctx->keys_alt, &ctx->vals,
                      &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob,
                      &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp, &ctx->item_log,
-                     &ctx->dBt, &ctx->dS2, &ctx->dAt, &ctx->dY2};
+                     &ctx->dBt, &ctx->dS2, &ctx->dAt, &ctx->dY2,
+                     &ctx->env_idx, &ctx->env_t, &ctx->env_q};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,

@@ -505,6 +505,79 @@ uint32_t next_pow2(uint32_t x) {
   return p;
 }
 
+// ---- response-function credible envelope (Fig. 1) --------------------------------
+// r(t) = 1 + (gamma/k2a) g(t; tD, tP, alpha) per accepted lp-ntPET draw, g the peak-normalised
+// gamma variate (eq:Bt P:90-94, R4); type-7 quantiles across the draws per time.
+// Operation for operation as the oracle (no FMA contraction).
+__device__ __forceinline__ double gamma_variate_d(double tD, double tP, double alpha, double t) {
+  if (t <= tD) return 0.0;
+  const double x = __ddiv_rn(__dsub_rn(t, tD), __dsub_rn(tP, tD));
+  return __dmul_rn(pow(x, alpha), exp(__dmul_rn(alpha, __dsub_rn(1.0, x))));
+}
+
+__global__ void response_envelope_kernel(const EnvelopeParams p, uint32_t np2, uint32_t wpc) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const uint32_t w = threadIdx.x >> 5;
+  const size_t per_warp = size_t(np2) * 28;
+  double* sc = reinterpret_cast<double*>(smem_raw + per_warp * w);  // [np2] values at one time
+  float4* prm = reinterpret_cast<float4*>(sc + np2);                 // [np2] (gamma, k2a, tD, tP)
+  float* pal = reinterpret_cast<float*>(prm + np2);                  // [np2] alpha
+  const float NANF = __int_as_float(0x7fc00000);
+  for (uint64_t v = uint64_t(blockIdx.x) * wpc + w; v < p.J; v += uint64_t(gridDim.x) * wpc) {
+    uint32_t cnt = 0;
+    for (uint32_t base = 0; base < p.n_acc; base += 32) {
+      const uint32_t a = base + lane;
+      bool mine = false;
+      float th[ABC_MAX_P];
+      if (a < p.n_acc) {
+        const uint64_t i = p.acc_idx[v * p.n_acc + a];
+        if (i >= p.N) {
+          atomicExch(p.bad, 1);
+        } else if (p.prior.m[model_index(p.prior, i)].kind == ABC_LPNTPET) {
+          draw_theta(p.prior, i, th);
+          mine = true;
+        }
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+      if (mine) {
+        const uint32_t pos = cnt + __popc(bal & ((1u << lane) - 1u));
+        prm[pos] = make_float4(th[3], th[2], th[4], th[5]);
+        pal[pos] = th[6];
+      }
+      cnt += __popc(bal);
+    }
+    __syncwarp();
+    uint32_t kp = 32;
+    while (kp < cnt) kp <<= 1;
+    for (uint32_t k = 0; k < p.T; ++k) {
+      float* o = p.q + (v * p.T + k) * 3;
+      if (cnt == 0) {
+        if (lane == 0) o[0] = o[1] = o[2] = NANF;
+        continue;
+      }
+      const double tk = p.t[k];
+      for (uint32_t a = lane; a < kp; a += 32) {
+        double r = __longlong_as_double(0x7ff0000000000000ll);
+        if (a < cnt) {
+          const float4 x = prm[a];
+          const double ratio = __ddiv_rn(double(x.x), double(x.y));
+          r = __dadd_rn(1.0, __dmul_rn(ratio, gamma_variate_d(x.z, x.w, pal[a], tk)));
+        }
+        sc[a] = r;
+      }
+      __syncwarp();
+      warp_sort_any(sc, nullptr, kp, lane);
+      if (lane == 0) {
+        o[0] = float(quantile7(sc, cnt, 0.025));
+        o[1] = float(quantile7(sc, cnt, 0.5));
+        o[2] = float(quantile7(sc, cnt, 0.975));
+      }
+      __syncwarp();
+    }
+  }
+}
+
 }  // namespace
 
 void launch_certify_reduce(const ReduceParams& p, cudaStream_t st) {
@@ -539,6 +612,24 @@ void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st) {
   uint64_t blocks = (p.J + 127) / 128;
   if (blocks == 0) return;
   eps_reduce_kernel<<<unsigned(blocks), 128, 0, st>>>(p);
+}
+
+void launch_response_envelope(const EnvelopeParams& p, cudaStream_t st) {
+  uint32_t np2 = next_pow2(p.n_acc);
+  if (np2 < 32) np2 = 32;
+  const size_t per_warp = size_t(np2) * 28;
+  uint32_t wpc = 8;
+  while (wpc > 1 && per_warp * wpc > 96 * 1024) wpc >>= 1;
+  const size_t smem = per_warp * wpc;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(response_envelope_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = smem;
+  }
+  uint64_t blocks = (p.J + wpc - 1) / wpc;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  if (blocks == 0) blocks = 1;
+  response_envelope_kernel<<<unsigned(blocks), wpc * 32, smem, st>>>(p, np2, wpc);
 }
 
 }  // namespace vpet

@@ -336,6 +336,18 @@ struct ReduceParams {
 };
 void launch_certify_reduce(const ReduceParams& p, cudaStream_t st);
 
+// Response-function envelope (Fig. 1): abc_response_envelope.
+struct EnvelopeParams {
+  const uint64_t* acc_idx;  // [J][n_acc]
+  uint64_t J, N;
+  uint32_t n_acc, T;
+  const double* t;          // [T] minutes
+  PriorDev prior;
+  float* q;                 // [J][T][3]
+  int* bad;                 // set when an index is >= N
+};
+void launch_response_envelope(const EnvelopeParams& p, cudaStream_t st);
+
 struct EpsReduceParams {
   const double* mom;
   uint64_t J;
