@@ -60,6 +60,9 @@ def lib():
         L.abc_set_frames.argtypes = [vp, vp, vp, vp, C.c_uint32]
         L.abc_run_voxels.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.POINTER(Result)]
         L.abc_model_select.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp]
+        L.abc_set_sim_noise.argtypes = [vp, C.c_double, C.c_double]
+        L.oracle_std_normal.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32]
+        L.oracle_std_normal.restype = C.c_double
         L.abc_response_envelope.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, C.c_uint32, C.c_uint32, vp]
         L.abc_last_error.argtypes = [vp]
         L.abc_last_error.restype = C.c_char_p
@@ -131,6 +134,10 @@ def gamma_variate(tD, tP, alpha, t) -> float:
 def feng(params, t) -> float:
     p = np.ascontiguousarray(params, dtype=np.float64)
     return float(lib().oracle_feng(_ptr(p), t))
+
+
+def std_normal(seed: int, i: int, f: int) -> float:
+    return float(lib().oracle_std_normal(seed, i, f))
 
 
 def quantile7(sorted_x, q) -> float:
@@ -219,6 +226,9 @@ class OracleContext:
         out = np.zeros(self.L, dtype=np.float64)
         self._check(lib().oracle_simulate(self._h, KINDS[kind], _ptr(th), _ptr(out)))
         return out
+
+    def set_sim_noise(self, ell, half_life_min=float("inf")):
+        self._check(lib().abc_set_sim_noise(self._h, float(ell), float(half_life_min)))
 
     def response_envelope(self, acc_idx, t):
         """J x T x 3 (2.5/50/97.5 %) of 1 + gamma/k2a g(t) over accepted lp-ntPET draws."""

@@ -54,6 +54,7 @@ struct abc_ctx {
   int prepared;      /* draw-independent grids below are valid */
   struct grid_s* gc; /* coarse grid: input knots U frame bounds */
   struct grid_s* gf; /* fine grid (lp-ntPET): {k delta} U knots U frame bounds */
+  double noise_ell, noise_lam; /* simulated-draw noise (abc_set_sim_noise); ell = 0: none */
   char err[256];
 };
 
@@ -445,6 +446,42 @@ abc_status oracle_simulate(const abc_ctx* ctx, int32_t kind, const float* theta,
 }
 
 /* Alg.1 l.1-3: the N x L matrix X, each value rounded to FP32 (RN). */
+/* Simulated-draw noise (P:218-220's model on the draws, as S:301; R17):
+ *   s = RN32(v + ell sigma z),  sigma = sqrt(max(v,0) e^{-lambda t} / dt) e^{lambda t},  t = frame mid,
+ *   z = Box-Muller of Philox4x32-10(ctr = {i_lo, i_hi, 2 + f/2, 'VPET'}, key = seed):
+ *   ua = u53(x0,x1), ub = u53(x2,x3), z = sqrt(-2 ln ua) cos(2 pi ub) (even f) | sin(2 pi ub) (odd f). */
+static double u53(uint32_t a, uint32_t b) {
+  uint64_t m = (((uint64_t)a << 32) | b) >> 11;
+  return (double)m * 0x1p-53 + 0x1p-54;
+}
+double oracle_std_normal(uint64_t seed, uint64_t i, uint32_t f) {
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t ctr[4] = {(uint32_t)i, (uint32_t)(i >> 32), 2u + f / 2u, CTR_TAG};
+  uint32_t x[4];
+  oracle_philox4x32_10(ctr, key, x);
+  double ua = u53(x[0], x[1]), ub = u53(x[2], x[3]);
+  double r = sqrt(-2.0 * log(ua));
+  double ang = 6.283185307179586 * ub;
+  return r * ((f & 1u) ? sin(ang) : cos(ang));
+}
+static float noisy_value(const abc_ctx* c, uint64_t i, uint32_t f, double v) {
+  if (c->noise_ell == 0.0) return (float)v;
+  double z = oracle_std_normal(c->cfg.seed, i, f);
+  double tm = c->fs[f] + 0.5 * c->fd[f];
+  double e = exp(c->noise_lam * tm);
+  double sig = sqrt(fmax(v, 0.0) / e / c->fd[f]) * e;
+  return (float)(v + c->noise_ell * sig * z);
+}
+
+abc_status abc_set_sim_noise(abc_ctx* c, double ell, double half_life_min) {
+  if (!c) return ABC_E_ARG;
+  if (!isfinite(ell) || ell < 0.0) return fail(c, ABC_E_ARG, "noise level must be finite and >= 0");
+  if (!(half_life_min > 0.0)) return fail(c, ABC_E_ARG, "half-life must be > 0 (may be +inf)");
+  c->noise_ell = ell;
+  c->noise_lam = log(2.0) / half_life_min;
+  return ABC_OK;
+}
+
 abc_status oracle_bank(const abc_ctx* ctx, float* bank) {
   if (!ctx || !ctx->have_input || !ctx->have_frames) return ABC_E_STATE;
   prepare((abc_ctx*)ctx);
@@ -458,7 +495,7 @@ abc_status oracle_bank(const abc_ctx* ctx, float* bank) {
     double v[ABC_MAX_L];
     draw_theta(&ctx->cfg, (uint64_t)i, &m, th);
     simulate(ctx, ctx->cfg.model[m].kind, th, v);
-    for (uint32_t f = 0; f < L; ++f) bank[(uint64_t)i * L + f] = (float)v[f];
+    for (uint32_t f = 0; f < L; ++f) bank[(uint64_t)i * L + f] = noisy_value(ctx, (uint64_t)i, f, v[f]);
   }
   return ABC_OK;
 }

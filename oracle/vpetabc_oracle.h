@@ -89,6 +89,10 @@ abc_status abc_model_select(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_
                             float* prob, int32_t* preferred);
 /* Response-function 95 % CrI envelope (Fig. 1): J x T x 3 quantiles of
  * 1 + gamma/k2a g(t) over each voxel's accepted lp-ntPET draws (host pointers only). */
+/* Simulated-draw noise (P:218-220 model on the draws): ell = 0 disables. */
+abc_status abc_set_sim_noise(abc_ctx* ctx, double ell, double half_life_min);
+/* the standard normal z_if of draw i, frame f (Box-Muller on Philox; see abc_set_sim_noise) */
+double oracle_std_normal(uint64_t seed, uint64_t i, uint32_t f);
 abc_status abc_response_envelope(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc,
                                  const double* t_min, uint32_t T, uint32_t ptr_flags, float* q);
 const char* abc_last_error(const abc_ctx* ctx);
