@@ -203,6 +203,17 @@ abc_status abc_get_stats(const abc_ctx* ctx, abc_stats* stats);
  * ABC_E_STATE before the first run; ABC_E_ARG if the rows are out of range. */
 abc_status abc_get_bank(const abc_ctx* ctx, float* out, uint64_t first, uint64_t count);
 
+/* Simulated-draw noise (the P:218-220 observation model applied to the draws, as
+ * SPEC S:301 does; R17).  From the next run on, each bank value becomes
+ *   s_if = RN32(v_f + ell sigma_f z_if),  sigma_f = sqrt(max(v_f, 0) e^{-lambda t_f} / dt_f) e^{lambda t_f},
+ * v_f the FP64 frame average, t_f the frame mid-time, lambda = ln 2 / half_life_min, and z_if a
+ * standard normal from Box-Muller on Philox4x32-10(ctr = {i_lo, i_hi, 2 + f/2, 'VPET'}, key = seed)
+ * (words x0..x3: ua = u53(x0, x1), ub = u53(x2, x3), u53(a, b) = ((a:b) >> 11 + 1/2) 2^-53;
+ * z = sqrt(-2 ln ua) cos(2 pi ub) for even f, sin(2 pi ub) for odd f).  ell = 0 (the default)
+ * is the noise-free method.  ABC_E_ARG: ell < 0 or non-finite, half_life_min <= 0 or NaN
+ * (+inf = no decay correction). */
+abc_status abc_set_sim_noise(abc_ctx* ctx, double ell, double half_life_min);
+
 /* Response-function 95 % credible envelope (Fig. 1).  For voxel j
  * and time t_min[k]: the type-7 2.5/50/97.5 % quantiles, over the voxel's accepted draws of an
  * lp-ntPET model, of the response function

@@ -155,6 +155,10 @@ class AbcContext:
     def model_select(self, tacs):
         return self.run_voxels(tacs, want=("prob", "preferred"))
 
+    def set_sim_noise(self, ell, half_life_min=float("inf")):
+        """Gaussian noise on the simulated draws (P:218-220 model, abc_set_sim_noise); ell = 0: none."""
+        self._check(self._lib.abc_set_sim_noise(self._h, float(ell), float(half_life_min)))
+
     def response_envelope(self, acc_idx, t):
         """J x T x 3 (2.5/50/97.5 %) quantiles of 1 + gamma/k2a g(t) over each voxel's accepted
         lp-ntPET draws (Fig. 1).  acc_idx: J x n uint64 (numpy, or a torch CUDA tensor:

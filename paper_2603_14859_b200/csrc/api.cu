@@ -68,6 +68,7 @@ struct abc_ctx {
   bool have_input = false, have_frames = false;
   int input_kind = ABC_INPUT_PWL;
   double feng[6] = {0, 0, 0, 0, 0, 0};
+  double noise_ell = 0.0, noise_lam = 0.0;  // abc_set_sim_noise
   std::vector<double> kt, kc;
   // frames
   uint32_t L = 0;
@@ -267,6 +268,8 @@ Tables make_tables(const abc_ctx* c, uint32_t LS) {
   T.fc = c->d_fc.as<double>();
   T.fframe = c->d_fframe.as<int>();
   T.feng = c->input_kind == ABC_INPUT_FENG;
+  T.noise_ell = c->noise_ell;
+  T.noise_lam = c->noise_lam;
   for (int k = 0; k < 6; ++k) T.fb[k] = c->feng[k];
   return T;
 }
@@ -974,6 +977,15 @@ abc_status abc_model_select(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_
   r.prob = prob;
   r.preferred = preferred;
   return abc_run_voxels(ctx, tacs, J, ptr_flags, &r);
+}
+
+abc_status abc_set_sim_noise(abc_ctx* ctx, double ell, double half_life_min) {
+  if (!ctx) return ABC_E_ARG;
+  if (!std::isfinite(ell) || ell < 0.0) return fail(ctx, ABC_E_ARG, "noise level must be finite and >= 0");
+  if (!(half_life_min > 0.0)) return fail(ctx, ABC_E_ARG, "half-life must be > 0 (may be +inf)");
+  ctx->noise_ell = ell;
+  ctx->noise_lam = std::log(2.0) / half_life_min;
+  return ABC_OK;
 }
 
 abc_status abc_response_envelope(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc,

@@ -20,20 +20,48 @@ namespace vpet {
 
 namespace {
 
+// Optional simulated-draw noise (abc_set_sim_noise; P:218-220 noise model applied to
+// the draws as in S:301; R17): value_f + ell sigma_f z_if with
+//   sigma_f = sqrt(max(value_f, 0) / e / dt_f) e,  e = exp(lambda t_f),  t_f = start_f + dt_f / 2,
+//   z_if = Box-Muller of Philox4x32-10(ctr = {i_lo, i_hi, 2 + f/2, 'VPET'}, key = seed):
+//   ua = u53(x0, x1), ub = u53(x2, x3), z = sqrt(-2 ln ua) (cos | sin)(2 pi ub) for even | odd f.
+// FP64, no contraction, then RN32.  ell = 0: exactly the noise-free RN32 value.
+struct DrawId {
+  uint64_t i;
+  uint32_t s0, s1;
+};
+__device__ __forceinline__ double u53(uint32_t a, uint32_t b) {
+  const uint64_t m = ((uint64_t(a) << 32) | b) >> 11;
+  return __dadd_rn(__dmul_rn(double(m), 1.1102230246251565e-16), 5.551115123125783e-17);  // (m + 1/2) 2^-53
+}
+__device__ __forceinline__ float emit(const Tables& T, const DrawId& d, int f, double v) {
+  if (T.noise_ell == 0.0) return __double2float_rn(v);
+  uint32_t x[4];
+  philox10(uint32_t(d.i), uint32_t(d.i >> 32), 2u + uint32_t(f) / 2u, kCtrTag, d.s0, d.s1, x);
+  const double ua = u53(x[0], x[1]), ub = u53(x[2], x[3]);
+  const double r = sqrt(__dmul_rn(-2.0, log(ua)));
+  const double ang = __dmul_rn(6.283185307179586, ub);
+  const double z = __dmul_rn(r, (f & 1) ? sin(ang) : cos(ang));
+  const double tm = __dadd_rn(T.fs[f], __dmul_rn(0.5, T.fdur[f]));
+  const double e = exp(__dmul_rn(T.noise_lam, tm));
+  const double sig = __dmul_rn(sqrt(__ddiv_rn(__ddiv_rn(fmax(v, 0.0), e), T.fdur[f])), e);
+  return __double2float_rn(__dadd_rn(v, __dmul_rn(__dmul_rn(T.noise_ell, sig), z)));
+}
+
 struct FrameAcc {
   int cur = -1;
   double A = 0.0, B = 0.0;
 };
 
 // ---- piecewise-linear input on a grid: both rates of the 2TCM at once ----
-__device__ void sim_2tcm_pwl(const Tables& T, double a1, double a2, double c1, double c2, double Vb,
+__device__ void sim_2tcm_pwl(const Tables& T, const DrawId& D, double a1, double a2, double c1, double c2, double Vb,
                              float* out) {
   double I1 = 0.0, I2 = 0.0;
   Phi P0{}, P1{}, Q0{}, Q1{};
   FrameAcc fa;
   auto flush = [&](int f) {
     double v = ((1.0 - Vb) * (c1 * fa.A + c2 * fa.B) + Vb * T.favg_in[f]) / T.fdur[f];
-    out[f] = __double2float_rn(v);
+    out[f] = emit(T, D, f, v);
   };
   for (uint32_t k = 0; k + 1 < T.G; ++k) {
     double t0 = T.gt[k], t1 = T.gt[k + 1];
@@ -99,22 +127,22 @@ __device__ inline double feng_conv(const double* b, double a, double ts, double 
          b[2] * intE(a, b[5], ts, te);
 }
 
-__device__ void sim_2tcm_feng(const Tables& T, double a1, double a2, double c1, double c2, double Vb, float* out) {
+__device__ void sim_2tcm_feng(const Tables& T, const DrawId& D, double a1, double a2, double c1, double c2, double Vb, float* out) {
   for (uint32_t f = 0; f < T.L; ++f) {
     double ts = T.fs[f], te = T.fe[f];
     double S1 = feng_conv(T.fb, a1, ts, te);
     double S2 = feng_conv(T.fb, a2, ts, te);
     double v = ((1.0 - Vb) * (c1 * S1 + c2 * S2) + Vb * T.favg_in[f]) / T.fdur[f];
-    out[f] = __double2float_rn(v);
+    out[f] = emit(T, D, f, v);
   }
 }
 
-__device__ void sim_mrtm(const Tables& T, double R1, double k2, double k2a, float* out) {
+__device__ void sim_mrtm(const Tables& T, const DrawId& D, double R1, double k2, double k2a, float* out) {
   double I = 0.0;
   FrameAcc fa;
   double kf = k2 - R1 * k2a;
   Phi P0{}, P1{};
-  auto flush = [&](int f) { out[f] = __double2float_rn((R1 * T.favg_in[f] + kf * fa.A) / T.fdur[f]); };
+  auto flush = [&](int f) { out[f] = emit(T, D, f, (R1 * T.favg_in[f] + kf * fa.A) / T.fdur[f]); };
   for (uint32_t k = 0; k + 1 < T.G; ++k) {
     double h = T.gt[k + 1] - T.gt[k];
     double ck = T.gc[k], ck1 = T.gc[k + 1];
@@ -138,12 +166,12 @@ __device__ void sim_mrtm(const Tables& T, double R1, double k2, double k2a, floa
   if (fa.cur >= 0) flush(fa.cur);
 }
 
-__device__ void sim_lpntpet(const Tables& T, const float* th, float* out) {
+__device__ void sim_lpntpet(const Tables& T, const DrawId& D, const float* th, float* out) {
   double R1 = th[0], k2 = th[1], k2a = th[2], gam = th[3], tD = th[4], tP = th[5], al = th[6];
   double inv = 1.0 / (tP - tD);
   double z = 0.0;
   FrameAcc fa;
-  auto flush = [&](int f) { out[f] = __double2float_rn((fa.A + R1 * T.favg_in[f]) / T.fdur[f]); };
+  auto flush = [&](int f) { out[f] = emit(T, D, f, (fa.A + R1 * T.favg_in[f]) / T.fdur[f]); };
   for (uint32_t k = 0; k + 1 < T.GF; ++k) {
     double t0 = T.ft[k], t1 = T.ft[k + 1];
     double h = t1 - t0;
@@ -178,6 +206,7 @@ __global__ void __launch_bounds__(128) bank_kernel(const BankParams p, const Pri
   int kind = prior.m[m].kind;
   float* out = p.bank + i * p.T.LS;
   const Tables& T = p.T;
+  const DrawId D{i, prior.seed_lo, prior.seed_hi};
   if (kind <= ABC_2TCM_REV) {
     double K1 = th[0], k2 = th[1], k3 = th[2], k4 = th[3], Vb = th[4];
     double s = k2 + k3 + k4;
@@ -187,12 +216,12 @@ __global__ void __launch_bounds__(128) bank_kernel(const BankParams p, const Pri
     double den = a2 - a1;
     double c1 = K1 * (k3 + k4 - a1) / den;
     double c2 = K1 * (a2 - k3 - k4) / den;
-    if (T.feng) sim_2tcm_feng(T, a1, a2, c1, c2, Vb, out);
-    else sim_2tcm_pwl(T, a1, a2, c1, c2, Vb, out);
+    if (T.feng) sim_2tcm_feng(T, D, a1, a2, c1, c2, Vb, out);
+    else sim_2tcm_pwl(T, D, a1, a2, c1, c2, Vb, out);
   } else if (kind == ABC_MRTM) {
-    sim_mrtm(T, th[0], th[1], th[2], out);
+    sim_mrtm(T, D, th[0], th[1], th[2], out);
   } else {
-    sim_lpntpet(T, th, out);
+    sim_lpntpet(T, D, th, out);
   }
   for (uint32_t f = T.L; f < T.LS; ++f) out[f] = 0.0f;
 }

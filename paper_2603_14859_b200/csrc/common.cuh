@@ -162,6 +162,8 @@ struct Tables {
   // Feng input
   int feng;
   double fb[6];
+  // simulated-draw noise (abc_set_sim_noise): ell = 0 disables
+  double noise_ell, noise_lam;
 };
 
 struct BankParams {
