@@ -34,8 +34,7 @@ __device__ __forceinline__ double u53(uint32_t a, uint32_t b) {
   const uint64_t m = ((uint64_t(a) << 32) | b) >> 11;
   return __dadd_rn(__dmul_rn(double(m), 1.1102230246251565e-16), 5.551115123125783e-17);  // (m + 1/2) 2^-53
 }
-__device__ __forceinline__ float emit(const Tables& T, const DrawId& d, int f, double v) {
-  if (T.noise_ell == 0.0) return __double2float_rn(v);
+__device__ __forceinline__ float emit_noisy(const Tables& T, const DrawId& d, int f, double v) {
   uint32_t x[4];
   philox10(uint32_t(d.i), uint32_t(d.i >> 32), 2u + uint32_t(f) / 2u, kCtrTag, d.s0, d.s1, x);
   const double ua = u53(x[0], x[1]), ub = u53(x[2], x[3]);
@@ -47,6 +46,12 @@ __device__ __forceinline__ float emit(const Tables& T, const DrawId& d, int f, d
   const double sig = __dmul_rn(sqrt(__ddiv_rn(__ddiv_rn(fmax(v, 0.0), e), T.fdur[f])), e);
   return __double2float_rn(__dadd_rn(v, __dmul_rn(__dmul_rn(T.noise_ell, sig), z)));
 }
+// NZ = false (ell = 0): a single rounding; the noisy variant is a separate kernel instance
+template <bool NZ>
+__device__ __forceinline__ float emit(const Tables& T, const DrawId& d, int f, double v) {
+  if constexpr (NZ) return emit_noisy(T, d, f, v);
+  else return __double2float_rn(v);
+}
 
 struct FrameAcc {
   int cur = -1;
@@ -54,6 +59,7 @@ struct FrameAcc {
 };
 
 // ---- piecewise-linear input on a grid: both rates of the 2TCM at once ----
+template <bool NZ>
 __device__ void sim_2tcm_pwl(const Tables& T, const DrawId& D, double a1, double a2, double c1, double c2, double Vb,
                              float* out) {
   double I1 = 0.0, I2 = 0.0;
@@ -61,7 +67,7 @@ __device__ void sim_2tcm_pwl(const Tables& T, const DrawId& D, double a1, double
   FrameAcc fa;
   auto flush = [&](int f) {
     double v = ((1.0 - Vb) * (c1 * fa.A + c2 * fa.B) + Vb * T.favg_in[f]) / T.fdur[f];
-    out[f] = emit(T, D, f, v);
+    out[f] = emit<NZ>(T, D, f, v);
   };
   for (uint32_t k = 0; k + 1 < T.G; ++k) {
     double t0 = T.gt[k], t1 = T.gt[k + 1];
@@ -127,22 +133,24 @@ __device__ inline double feng_conv(const double* b, double a, double ts, double 
          b[2] * intE(a, b[5], ts, te);
 }
 
+template <bool NZ>
 __device__ void sim_2tcm_feng(const Tables& T, const DrawId& D, double a1, double a2, double c1, double c2, double Vb, float* out) {
   for (uint32_t f = 0; f < T.L; ++f) {
     double ts = T.fs[f], te = T.fe[f];
     double S1 = feng_conv(T.fb, a1, ts, te);
     double S2 = feng_conv(T.fb, a2, ts, te);
     double v = ((1.0 - Vb) * (c1 * S1 + c2 * S2) + Vb * T.favg_in[f]) / T.fdur[f];
-    out[f] = emit(T, D, f, v);
+    out[f] = emit<NZ>(T, D, f, v);
   }
 }
 
+template <bool NZ>
 __device__ void sim_mrtm(const Tables& T, const DrawId& D, double R1, double k2, double k2a, float* out) {
   double I = 0.0;
   FrameAcc fa;
   double kf = k2 - R1 * k2a;
   Phi P0{}, P1{};
-  auto flush = [&](int f) { out[f] = emit(T, D, f, (R1 * T.favg_in[f] + kf * fa.A) / T.fdur[f]); };
+  auto flush = [&](int f) { out[f] = emit<NZ>(T, D, f, (R1 * T.favg_in[f] + kf * fa.A) / T.fdur[f]); };
   for (uint32_t k = 0; k + 1 < T.G; ++k) {
     double h = T.gt[k + 1] - T.gt[k];
     double ck = T.gc[k], ck1 = T.gc[k + 1];
@@ -166,12 +174,13 @@ __device__ void sim_mrtm(const Tables& T, const DrawId& D, double R1, double k2,
   if (fa.cur >= 0) flush(fa.cur);
 }
 
+template <bool NZ>
 __device__ void sim_lpntpet(const Tables& T, const DrawId& D, const float* th, float* out) {
   double R1 = th[0], k2 = th[1], k2a = th[2], gam = th[3], tD = th[4], tP = th[5], al = th[6];
   double inv = 1.0 / (tP - tD);
   double z = 0.0;
   FrameAcc fa;
-  auto flush = [&](int f) { out[f] = emit(T, D, f, (fa.A + R1 * T.favg_in[f]) / T.fdur[f]); };
+  auto flush = [&](int f) { out[f] = emit<NZ>(T, D, f, (fa.A + R1 * T.favg_in[f]) / T.fdur[f]); };
   for (uint32_t k = 0; k + 1 < T.GF; ++k) {
     double t0 = T.ft[k], t1 = T.ft[k + 1];
     double h = t1 - t0;
@@ -198,6 +207,7 @@ __device__ void sim_lpntpet(const Tables& T, const DrawId& D, const float* th, f
   if (fa.cur >= 0) flush(fa.cur);
 }
 
+template <bool NZ>
 __global__ void __launch_bounds__(128) bank_kernel(const BankParams p, const PriorDev prior) {
   uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= p.N) return;
@@ -216,12 +226,12 @@ __global__ void __launch_bounds__(128) bank_kernel(const BankParams p, const Pri
     double den = a2 - a1;
     double c1 = K1 * (k3 + k4 - a1) / den;
     double c2 = K1 * (a2 - k3 - k4) / den;
-    if (T.feng) sim_2tcm_feng(T, D, a1, a2, c1, c2, Vb, out);
-    else sim_2tcm_pwl(T, D, a1, a2, c1, c2, Vb, out);
+    if (T.feng) sim_2tcm_feng<NZ>(T, D, a1, a2, c1, c2, Vb, out);
+    else sim_2tcm_pwl<NZ>(T, D, a1, a2, c1, c2, Vb, out);
   } else if (kind == ABC_MRTM) {
-    sim_mrtm(T, D, th[0], th[1], th[2], out);
+    sim_mrtm<NZ>(T, D, th[0], th[1], th[2], out);
   } else {
-    sim_lpntpet(T, D, th, out);
+    sim_lpntpet<NZ>(T, D, th, out);
   }
   for (uint32_t f = T.L; f < T.LS; ++f) out[f] = 0.0f;
 }
@@ -235,7 +245,8 @@ __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, uint64_t n) {
 
 void launch_bank(const BankParams& p, const PriorDev& prior, cudaStream_t st) {
   uint64_t blocks = (p.N + 127) / 128;
-  bank_kernel<<<unsigned(blocks), 128, 0, st>>>(p, prior);
+  if (p.T.noise_ell != 0.0) bank_kernel<true><<<unsigned(blocks), 128, 0, st>>>(p, prior);
+  else bank_kernel<false><<<unsigned(blocks), 128, 0, st>>>(p, prior);
 }
 
 void launch_fill_u32(uint32_t* p, uint32_t v, uint64_t n, cudaStream_t st) {
