@@ -85,6 +85,7 @@ struct abc_ctx {
   DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp, item_log;
   DevBuf dBt, dS2, dAt, dY2;  // ABC_FLAG_DENSE_TC operands (dense_tc.cu)
   DevBuf env_idx, env_t, env_q;  // abc_response_envelope staging
+  DevBuf proj;                   // [N][kNPC] bank projections (order stage)
   abc_stats stats{};
   bool bank_valid = false;
   uint64_t mem_sig[6] = {~0ull, 0, 0, 0, 0, 0};  // (J, N, flags, ptr_flags, n, L) of the last passed memory check
@@ -580,7 +581,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (nparts == 0) nparts = 1;
   if (dense) nparts = 2;  // the two column halves of each draw tile (dense_tc.cu)
   const size_t vsort_tmp = tree ? voxel_sort_temp_bytes(J) : 0;
-  if (tree) need += N * (8 + 8 + 4 + 4 + 4) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper + nhyper);
+  if (tree) need += N * (8 + 8 + 4 + 4 + 4 + 4 * kNPC) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper + nhyper);
   if (tree) need += 24 * J + vsort_tmp;
   if (!eps) need += (size_t(8) * heap_stride(std::max<uint32_t>(K, 1)) + 4) * J * nparts + 4 * J;  // heaps
   need += size_t(12) * J * (n ? n : 1);                  // exact heaps (fallback)
@@ -614,6 +615,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(ctx->pcs.ensure(sizeof(float) * kNPC * kMaxLP));
     CK(ctx->pminmax.ensure(sizeof(unsigned int) * 2 * kNPC));
     CK(ctx->keys.ensure(8 * N));
+    CK(ctx->proj.ensure(sizeof(float) * kNPC * N));
     CK(ctx->keys_alt.ensure(8 * N));
     CK(ctx->vals.ensure(4 * N));
     CK(ctx->order.ensure(4 * N));
@@ -735,6 +737,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       op.cov = ctx->cov.as<double>();
       op.pcs = ctx->pcs.as<float>();
       op.pminmax = ctx->pminmax.as<unsigned int>();
+      op.proj = ctx->proj.as<float>();
       op.keys = ctx->keys.as<unsigned long long>();
       op.keys_alt = ctx->keys_alt.as<unsigned long long>();
       op.vals = ctx->vals.as<uint32_t>();
@@ -1051,7 +1054,7 @@ void abc_destroy(abc_ctx* ctx) {
                      &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob,
                      &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp, &ctx->item_log,
                      &ctx->dBt, &ctx->dS2, &ctx->dAt, &ctx->dY2,
-                     &ctx->env_idx, &ctx->env_t, &ctx->env_q};
+                     &ctx->env_idx, &ctx->env_t, &ctx->env_q, &ctx->proj};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,

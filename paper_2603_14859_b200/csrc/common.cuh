@@ -190,6 +190,7 @@ struct OrderParams {
   double* cov;        // [LP][LP]
   float* pcs;         // [kNPC][LP]
   unsigned int* pminmax;  // [kNPC][2] ordered-int min/max of the projections
+  float* proj;            // [N][kNPC] principal-axis projections (written by proj_minmax, read by key)
   unsigned long long* keys;      // [N]
   unsigned long long* keys_alt;  // [N]
   uint32_t* vals;     // [N]

@@ -219,6 +219,10 @@ __global__ void __launch_bounds__(256) proj_minmax_kernel(const OrderParams p) {
     project(p, sm, i, pr);
 #pragma unroll
     for (int c = 0; c < kNPC; ++c) { lo[c] = fminf(lo[c], pr[c]); hi[c] = fmaxf(hi[c], pr[c]); }
+    // kept for key_kernel (one pass over the bank instead of two)
+    if constexpr (kNPC == 4) reinterpret_cast<float4*>(p.proj)[i] = make_float4(pr[0], pr[1], pr[2], pr[3]);
+    else
+      for (int c = 0; c < kNPC; ++c) p.proj[i * kNPC + c] = pr[c];
   }
 #pragma unroll
   for (int c = 0; c < kNPC; ++c) {
@@ -275,7 +279,12 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
   __syncthreads();
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < p.N; i += uint64_t(gridDim.x) * blockDim.x) {
     float pr[kNPC];
-    project(p, sm, i, pr);
+    if constexpr (kNPC == 4) {
+      const float4 v = reinterpret_cast<const float4*>(p.proj)[i];
+      pr[0] = v.x; pr[1] = v.y; pr[2] = v.z; pr[3] = v.w;
+    } else {
+      for (int c = 0; c < kNPC; ++c) pr[c] = p.proj[i * kNPC + c];
+    }
     unsigned long long key = 0;
 #pragma unroll
     for (int c = 0; c < kNPC; ++c) {
@@ -317,11 +326,23 @@ __global__ void __launch_bounds__(32 * kPermWarps) permute_kernel(const OrderPar
     }
     sidx[wid][lane] = myi;
     __syncwarp();
-    for (uint32_t e = lane; e < nr * Q; e += 32) {  // gather: element e = (row e / Q, float4 e % Q)
-      const uint32_t r = e / Q, q = e % Q;
-      const float4 x = __ldg(reinterpret_cast<const float4*>(p.bank + uint64_t(sidx[wid][r]) * LS) + q);
-      float* d = rows + r * stride + 4 * q;
-      d[0] = x.x; d[1] = x.y; d[2] = x.z; d[3] = x.w;
+    // gather: element e = (row e / Q, float4 e % Q); eight independent 16-B loads in flight per lane
+    for (uint32_t e0 = lane; e0 < nr * Q; e0 += 32 * 8) {
+      float4 x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t e = e0 + 32u * u;
+        if (e < nr * Q)
+          x[u] = __ldg(reinterpret_cast<const float4*>(p.bank + uint64_t(sidx[wid][e / Q]) * LS) + e % Q);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t e = e0 + 32u * u;
+        if (e < nr * Q) {
+          float* d = rows + (e / Q) * stride + 4 * (e % Q);
+          d[0] = x[u].x; d[1] = x[u].y; d[2] = x[u].z; d[3] = x[u].w;
+        }
+      }
     }
     __syncwarp();
     for (uint32_t k0 = 0; k0 < p.LP; k0 += 32) {
