@@ -78,6 +78,7 @@ struct abc_ctx {
   // device tables
   bool dirty = true;
   uint32_t G = 0, GF = 0;
+  DevBuf d_finv;  // [L] 1 / frame duration (the bank multiplies instead of dividing)
   DevBuf d_fdur, d_fs, d_fe, d_favg, d_w, d_wsc, d_gt, d_gc, d_gframe, d_gcode, d_ft, d_fc, d_fframe;
   // work buffers
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
@@ -207,6 +208,11 @@ abc_status build_tables(abc_ctx* ctx) {
     else wsc[f] = ctx->w[f];
   }
   CK(upload(ctx->d_fdur, ctx->fd));
+  {
+    std::vector<double> finv(ctx->fd.size());
+    for (size_t f = 0; f < finv.size(); ++f) finv[f] = 1.0 / ctx->fd[f];
+    CK(upload(ctx->d_finv, finv));
+  }
   CK(upload(ctx->d_fs, ctx->fs));
   CK(upload(ctx->d_fe, fe));
   CK(upload(ctx->d_favg, favg));
@@ -255,6 +261,7 @@ Tables make_tables(const abc_ctx* c, uint32_t LS) {
   T.L = c->L;
   T.LS = LS;
   T.fdur = c->d_fdur.as<double>();
+  T.finv = c->d_finv.as<double>();
   T.fs = c->d_fs.as<double>();
   T.fe = c->d_fe.as<double>();
   T.favg_in = c->d_favg.as<double>();
@@ -1056,7 +1063,7 @@ void abc_destroy(abc_ctx* ctx) {
                      &ctx->dBt, &ctx->dS2, &ctx->dAt, &ctx->dY2,
                      &ctx->env_idx, &ctx->env_t, &ctx->env_q, &ctx->proj};
   for (DevBuf* b : bufs2) b->release();
-  DevBuf* bufs[] = {&ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
+  DevBuf* bufs[] = {&ctx->d_finv, &ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,
                     &ctx->bank,   &ctx->bankp, &ctx->var,    &ctx->perm,   &ctx->wsp,        &ctx->heap,
                     &ctx->heap_cnt, &ctx->tacs, &ctx->fb_list, &ctx->fb_len, &ctx->work,     &ctx->hd,

@@ -10,6 +10,8 @@
 //     S_f(a) = int_f (C_p (x) e^{-a.}) dt: exact recurrences on the PWL grid, or the Feng
 //     closed form.
 //   MRTM (eq:lp-ntPET with gamma = 0): value_f = [R1 int_f C_r + (k2 - R1 k2a) S_f(k2a)]/dt_f.
+//   (/ dt_f is applied as * RN64(1/dt_f), rounded on the host: at most an FP64 ulp from the oracle's
+//   division, which changes RN32 only for a value within that ulp of an FP32 rounding tie.)
 //   lp-ntPET (eq:lp-ntPET, eq:Bt): z = C_t - R1 C_r, z' = (k2 - R1 a) C_r - a z,
 //     a(t) = k2a + gamma g(t) frozen at each substep midpoint (R4).
 #include <cfloat>
@@ -66,7 +68,7 @@ __device__ void sim_2tcm_pwl(const Tables& T, const DrawId& D, double a1, double
   Phi P0{}, P1{}, Q0{}, Q1{};
   FrameAcc fa;
   auto flush = [&](int f) {
-    double v = ((1.0 - Vb) * (c1 * fa.A + c2 * fa.B) + Vb * T.favg_in[f]) / T.fdur[f];
+    double v = ((1.0 - Vb) * (c1 * fa.A + c2 * fa.B) + Vb * T.favg_in[f]) * T.finv[f];
     out[f] = emit<NZ>(T, D, f, v);
   };
   for (uint32_t k = 0; k + 1 < T.G; ++k) {
@@ -139,7 +141,7 @@ __device__ void sim_2tcm_feng(const Tables& T, const DrawId& D, double a1, doubl
     double ts = T.fs[f], te = T.fe[f];
     double S1 = feng_conv(T.fb, a1, ts, te);
     double S2 = feng_conv(T.fb, a2, ts, te);
-    double v = ((1.0 - Vb) * (c1 * S1 + c2 * S2) + Vb * T.favg_in[f]) / T.fdur[f];
+    double v = ((1.0 - Vb) * (c1 * S1 + c2 * S2) + Vb * T.favg_in[f]) * T.finv[f];
     out[f] = emit<NZ>(T, D, f, v);
   }
 }
@@ -150,7 +152,7 @@ __device__ void sim_mrtm(const Tables& T, const DrawId& D, double R1, double k2,
   FrameAcc fa;
   double kf = k2 - R1 * k2a;
   Phi P0{}, P1{};
-  auto flush = [&](int f) { out[f] = emit<NZ>(T, D, f, (R1 * T.favg_in[f] + kf * fa.A) / T.fdur[f]); };
+  auto flush = [&](int f) { out[f] = emit<NZ>(T, D, f, (R1 * T.favg_in[f] + kf * fa.A) * T.finv[f]); };
   for (uint32_t k = 0; k + 1 < T.G; ++k) {
     double h = T.gt[k + 1] - T.gt[k];
     double ck = T.gc[k], ck1 = T.gc[k + 1];
@@ -180,7 +182,7 @@ __device__ void sim_lpntpet(const Tables& T, const DrawId& D, const float* th, f
   double inv = 1.0 / (tP - tD);
   double z = 0.0;
   FrameAcc fa;
-  auto flush = [&](int f) { out[f] = emit<NZ>(T, D, f, (fa.A + R1 * T.favg_in[f]) / T.fdur[f]); };
+  auto flush = [&](int f) { out[f] = emit<NZ>(T, D, f, (fa.A + R1 * T.favg_in[f]) * T.finv[f]); };
   for (uint32_t k = 0; k + 1 < T.GF; ++k) {
     double t0 = T.ft[k], t1 = T.ft[k + 1];
     double h = t1 - t0;

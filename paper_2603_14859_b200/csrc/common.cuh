@@ -144,6 +144,7 @@ struct Tables {
   // frames (acquisition order)
   uint32_t L, LS;          // frames, padded stride of the exact bank
   const double* fdur;      // [L]
+  const double* finv;      // [L] 1 / fdur (host-rounded)
   const double* fs;        // [L] starts
   const double* fe;        // [L] ends
   const double* favg_in;   // [L] int_frame C_in dt (draw independent)
