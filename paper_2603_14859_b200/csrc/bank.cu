@@ -84,21 +84,24 @@ __device__ void sim_2tcm_pwl(const Tables& T, const DrawId& D, double a1, double
       Phi np = phi_all(a1 * h), nq = phi_all(a2 * h);
       if (slot == 0) { P0 = np; Q0 = nq; } else { P1 = np; Q1 = nq; }
     }
-    const Phi& p = slot == 0 ? P0 : P1;
-    const Phi& q = slot == 0 ? Q0 : Q1;
-    double dc = ck1 - ck;
-    double s1 = h * p.p1 * I1 + h * h * (ck1 * p.ps - dc * p.om);
-    double s2 = h * q.p1 * I2 + h * h * (ck1 * q.ps - dc * q.om);
-    if (f != fa.cur) {
-      if (fa.cur >= 0) flush(fa.cur);
-      fa.cur = f;
-      fa.A = 0.0;
-      fa.B = 0.0;
-    }
-    fa.A += s1;
-    fa.B += s2;
-    I1 = p.e * I1 + h * (ck * p.ch + ck1 * p.ps);
-    I2 = q.e * I2 + h * (ck * q.ch + ck1 * q.ps);
+    // slot is warp-uniform (one schedule for all draws): branch instead of selecting 10 doubles
+    auto body = [&](const Phi& p, const Phi& q) {
+      double dc = ck1 - ck;
+      double s1 = h * p.p1 * I1 + h * h * (ck1 * p.ps - dc * p.om);
+      double s2 = h * q.p1 * I2 + h * h * (ck1 * q.ps - dc * q.om);
+      if (f != fa.cur) {
+        if (fa.cur >= 0) flush(fa.cur);
+        fa.cur = f;
+        fa.A = 0.0;
+        fa.B = 0.0;
+      }
+      fa.A += s1;
+      fa.B += s2;
+      I1 = p.e * I1 + h * (ck * p.ch + ck1 * p.ps);
+      I2 = q.e * I2 + h * (ck * q.ch + ck1 * q.ps);
+    };
+    if (slot == 0) body(P0, Q0);
+    else body(P1, Q1);
   }
   if (fa.cur >= 0) flush(fa.cur);
 }
@@ -163,15 +166,18 @@ __device__ void sim_mrtm(const Tables& T, const DrawId& D, double R1, double k2,
       Phi np = phi_all(k2a * h);
       if (slot == 0) P0 = np; else P1 = np;
     }
-    const Phi& p = slot == 0 ? P0 : P1;
-    double s = h * p.p1 * I + h * h * (ck1 * p.ps - (ck1 - ck) * p.om);
-    if (f != fa.cur) {
-      if (fa.cur >= 0) flush(fa.cur);
-      fa.cur = f;
-      fa.A = 0.0;
-    }
-    fa.A += s;
-    I = p.e * I + h * (ck * p.ch + ck1 * p.ps);
+    auto body = [&](const Phi& p) {  // slot is warp-uniform: branch, not select
+      double s = h * p.p1 * I + h * h * (ck1 * p.ps - (ck1 - ck) * p.om);
+      if (f != fa.cur) {
+        if (fa.cur >= 0) flush(fa.cur);
+        fa.cur = f;
+        fa.A = 0.0;
+      }
+      fa.A += s;
+      I = p.e * I + h * (ck * p.ch + ck1 * p.ps);
+    };
+    if (slot == 0) body(P0);
+    else body(P1);
   }
   if (fa.cur >= 0) flush(fa.cur);
 }
