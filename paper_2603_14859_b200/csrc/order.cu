@@ -9,6 +9,8 @@
 // changes which draws are looked at first; selection is by (D, original index) keys.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace vpet {
@@ -507,7 +509,11 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
     key_kernel<<<148 * 8, 256, 0, st>>>(p);
     *launches += 4;
     size_t tb = p.sort_temp_bytes;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(p.sort_temp, tb, p.keys, p.keys_alt, p.vals, p.order, int(p.N), 0,
+    // the lowest 8 key bits (the two finest Morton levels of each axis) are not sorted: one radix
+    // pass less, same scan time (measured: 0 / 8 / 16 bits -> scan 19.6 / 19.5 / 20.3 ms); the
+    // order is free.  Tuning knob VPET_SORT_LO.
+    static const int lo_bit = getenv("VPET_SORT_LO") ? atoi(getenv("VPET_SORT_LO")) : 8;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(p.sort_temp, tb, p.keys, p.keys_alt, p.vals, p.order, int(p.N), lo_bit,
                                                     kNPC * kMBits, st);
     if (e != cudaSuccess) return e;
     *launches += 4;  // onesweep: histogram + passes (approximate count of CUB launches)
