@@ -287,7 +287,10 @@ __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* c
   }
 }
 
-__global__ void certify_reduce_kernel(const ReduceParams p, uint32_t Kp, uint32_t np2, uint32_t wpc) {
+#ifndef CERT_MINB
+#define CERT_MINB 4  // 4 CTAs of 8 warps per SM (<= 64 registers)
+#endif
+__global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const ReduceParams p, uint32_t Kp, uint32_t np2, uint32_t wpc) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const uint32_t w = threadIdx.x >> 5;
