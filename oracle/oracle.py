@@ -61,6 +61,7 @@ def lib():
         L.abc_run_voxels.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.POINTER(Result)]
         L.abc_model_select.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, vp]
         L.abc_set_sim_noise.argtypes = [vp, C.c_double, C.c_double]
+        L.abc_patlak.argtypes = [vp, vp, C.c_uint64, C.c_double, C.c_uint32, vp, vp]
         L.oracle_std_normal.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32]
         L.oracle_std_normal.restype = C.c_double
         L.abc_response_envelope.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, C.c_uint32, C.c_uint32, vp]
@@ -226,6 +227,15 @@ class OracleContext:
         out = np.zeros(self.L, dtype=np.float64)
         self._check(lib().oracle_simulate(self._h, KINDS[kind], _ptr(th), _ptr(out)))
         return out
+
+    def patlak(self, tacs, t_star):
+        """(K_i, intercept) per voxel: OLS Patlak line over frames with mid-time >= t_star."""
+        y = np.ascontiguousarray(tacs, dtype=np.float32)
+        J = y.shape[0]
+        ki = np.zeros(J, dtype=np.float32)
+        v0 = np.zeros(J, dtype=np.float32)
+        self._check(lib().abc_patlak(self._h, _ptr(y), J, float(t_star), 0, _ptr(ki), _ptr(v0)))
+        return ki, v0
 
     def set_sim_noise(self, ell, half_life_min=float("inf")):
         self._check(lib().abc_set_sim_noise(self._h, float(ell), float(half_life_min)))

@@ -848,6 +848,81 @@ abc_status abc_response_envelope(abc_ctx* c, const uint64_t* acc_idx, uint64_t J
   return ABC_OK;
 }
 
+/* Patlak graphical analysis (the clinical K_i reference of P:282, Patlak 1983; SURVEY §8f-4;
+ * DESIGN.md R18).  For the frames with mid-time t_f >= t_star:
+ *   Cp_f = int_frame Cp / dt_f (frame average of the input), X_f = int_0^{t_f} Cp,
+ *   x_f = X_f / Cp_f,  z_f = y_f / Cp_f,
+ * and the ordinary least-squares line z = K_i x + V0 (centred two-pass formulas, FP64).
+ * NaN when fewer than two frames qualify.  Host pointers only. */
+static double input_at(const abc_ctx* c, double t) {
+  return c->input_kind == ABC_INPUT_FENG ? oracle_feng(c->feng, t) : pwl_value(c->kt, c->kc, c->nk, t);
+}
+static double input_integral(const abc_ctx* c, double t0, double t1) {
+  if (c->input_kind == ABC_INPUT_FENG) return feng_frame(c->feng, t0, t1);
+  /* piecewise linear: trapezoids between t0, the knots inside (t0, t1), and t1 (exact) */
+  double s = 0.0, a = t0, va = input_at(c, t0);
+  for (uint32_t k = 0; k < c->nk; ++k) {
+    if (c->kt[k] <= t0) continue;
+    if (c->kt[k] >= t1) break;
+    double vb = c->kc[k];
+    s += 0.5 * (c->kt[k] - a) * (va + vb);
+    a = c->kt[k];
+    va = vb;
+  }
+  s += 0.5 * (t1 - a) * (va + input_at(c, t1));
+  return s;
+}
+abc_status abc_patlak(abc_ctx* c, const float* tacs, uint64_t J, double t_star, uint32_t ptr_flags, float* ki,
+                      float* intercept) {
+  if (!c) return ABC_E_ARG;
+  if (!c->have_input || !c->have_frames) return fail(c, ABC_E_STATE, "input function and frames must be set");
+  if (ptr_flags != 0) return fail(c, ABC_E_ARG, "the oracle takes host pointers only");
+  if (J == 0) return ABC_OK;
+  if (!tacs || !ki || !isfinite(t_star)) return fail(c, ABC_E_ARG, "bad Patlak arguments");
+  uint32_t L = c->L;
+  double* x = (double*)malloc(sizeof(double) * L);
+  double* cp = (double*)malloc(sizeof(double) * L);
+  int* use = (int*)malloc(sizeof(int) * L);
+  uint32_t m = 0;
+  for (uint32_t f = 0; f < L; ++f) {
+    double tm = c->fs[f] + 0.5 * c->fd[f];
+    use[f] = tm >= t_star;
+    cp[f] = input_integral(c, c->fs[f], c->fs[f] + c->fd[f]) / c->fd[f];
+    x[f] = input_integral(c, 0.0, tm) / cp[f];
+    m += use[f];
+  }
+  for (uint64_t j = 0; j < J; ++j) {
+    double slope = NAN, icpt = NAN;
+    if (m >= 2) {
+      double xb = 0.0, zb = 0.0;
+      for (uint32_t f = 0; f < L; ++f)
+        if (use[f]) {
+          xb += x[f];
+          zb += (double)tacs[j * L + f] / cp[f];
+        }
+      xb /= m;
+      zb /= m;
+      double sxx = 0.0, sxz = 0.0;
+      for (uint32_t f = 0; f < L; ++f)
+        if (use[f]) {
+          double dx = x[f] - xb, dz = (double)tacs[j * L + f] / cp[f] - zb;
+          sxx += dx * dx;
+          sxz += dx * dz;
+        }
+      if (sxx > 0.0) {
+        slope = sxz / sxx;
+        icpt = zb - slope * xb;
+      }
+    }
+    ki[j] = (float)slope;
+    if (intercept) intercept[j] = (float)icpt;
+  }
+  free(x);
+  free(cp);
+  free(use);
+  return ABC_OK;
+}
+
 const char* abc_last_error(const abc_ctx* c) { return c ? c->err : "null context"; }
 
 void abc_destroy(abc_ctx* c) {

@@ -93,6 +93,9 @@ abc_status abc_model_select(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_
 abc_status abc_set_sim_noise(abc_ctx* ctx, double ell, double half_life_min);
 /* the standard normal z_if of draw i, frame f (Box-Muller on Philox; see abc_set_sim_noise) */
 double oracle_std_normal(uint64_t seed, uint64_t i, uint32_t f);
+/* Patlak K_i and intercept per voxel from the frames with mid-time >= t_star (R18). */
+abc_status abc_patlak(abc_ctx* ctx, const float* tacs, uint64_t J, double t_star_min, uint32_t ptr_flags,
+                      float* ki, float* intercept);
 abc_status abc_response_envelope(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc,
                                  const double* t_min, uint32_t T, uint32_t ptr_flags, float* q);
 const char* abc_last_error(const abc_ctx* ctx);
