@@ -203,6 +203,17 @@ abc_status abc_get_stats(const abc_ctx* ctx, abc_stats* stats);
  * ABC_E_STATE before the first run; ABC_E_ARG if the rows are out of range. */
 abc_status abc_get_bank(const abc_ctx* ctx, float* out, uint64_t first, uint64_t count);
 
+/* Patlak K_i map (the clinical reference K_i image of P:282; Patlak 1983; SURVEY.md §8f-4;
+ * DESIGN.md R18).  For each voxel, the least-squares line z = K_i x + V0 through the frames
+ * whose mid-time t_f >= t_star_min, with x_f = (int_0^{t_f} C_in) / Cp_f, z_f = y_f / Cp_f and
+ * Cp_f the frame average of the context's input function (FP64).  tacs: J x L FP32 (host, or
+ * device with ABC_PTR_TACS_DEVICE); ki, intercept (may be NULL): J FP32 (host, or device with
+ * ABC_PTR_OUT_DEVICE).  NaN when fewer than two frames qualify.  ABC_E_STATE before the input
+ * function and frames are set; ABC_E_ARG for NULL tacs/ki or a non-finite t_star_min.  Blocks until
+ * the outputs are complete. */
+abc_status abc_patlak(abc_ctx* ctx, const float* tacs, uint64_t J, double t_star_min, uint32_t ptr_flags,
+                      float* ki, float* intercept);
+
 /* Simulated-draw noise (the P:218-220 observation model applied to the draws, as
  * SPEC S:301 does; R17).  From the next run on, each bank value becomes
  *   s_if = RN32(v_f + ell sigma_f z_if),  sigma_f = sqrt(max(v_f, 0) e^{-lambda t_f} / dt_f) e^{lambda t_f},

@@ -155,6 +155,25 @@ class AbcContext:
     def model_select(self, tacs):
         return self.run_voxels(tacs, want=("prob", "preferred"))
 
+    def patlak(self, tacs, t_star):
+        """(K_i, intercept) per voxel: least-squares Patlak line over the frames with mid-time >=
+        t_star (abc_patlak).  numpy host arrays, or a torch CUDA tensor (device outputs)."""
+        if type(tacs).__module__.startswith("torch") and tacs.is_cuda:
+            import torch
+            J = int(tacs.shape[0])
+            ki = torch.empty(J, dtype=torch.float32, device=tacs.device)
+            v0 = torch.empty(J, dtype=torch.float32, device=tacs.device)
+            self._check(self._lib.abc_patlak(self._h, C.c_void_p(tacs.data_ptr()), J, float(t_star),
+                                             A.PTR_TACS_DEVICE | A.PTR_OUT_DEVICE, C.c_void_p(ki.data_ptr()),
+                                             C.c_void_p(v0.data_ptr())))
+            return ki, v0
+        y = np.ascontiguousarray(tacs, dtype=np.float32)
+        J = y.shape[0]
+        ki = np.zeros(J, dtype=np.float32)
+        v0 = np.zeros(J, dtype=np.float32)
+        self._check(self._lib.abc_patlak(self._h, y.ctypes.data, J, float(t_star), 0, ki.ctypes.data, v0.ctypes.data))
+        return ki, v0
+
     def set_sim_noise(self, ell, half_life_min=float("inf")):
         """Gaussian noise on the simulated draws (P:218-220 model, abc_set_sim_noise); ell = 0: none."""
         self._check(self._lib.abc_set_sim_noise(self._h, float(ell), float(half_life_min)))

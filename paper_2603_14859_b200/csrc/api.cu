@@ -87,6 +87,7 @@ struct abc_ctx {
   DevBuf dBt, dS2, dAt, dY2;  // ABC_FLAG_DENSE_TC operands (dense_tc.cu)
   DevBuf env_idx, env_t, env_q;  // abc_response_envelope staging
   DevBuf proj;                   // [N][kNPC] bank projections (order stage)
+  DevBuf pat_ab;                 // abc_patlak frame coefficients [2][L]
   abc_stats stats{};
   bool bank_valid = false;
   uint64_t mem_sig[6] = {~0ull, 0, 0, 0, 0, 0};  // (J, N, flags, ptr_flags, n, L) of the last passed memory check
@@ -989,6 +990,82 @@ abc_status abc_model_select(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_
   return abc_run_voxels(ctx, tacs, J, ptr_flags, &r);
 }
 
+// int_t0^t1 of the input function (host, FP64): Feng closed form, or exact trapezoids of the PWL
+// curve between t0, the knots inside and t1 (held at the last value after the last knot).
+static double input_integral_host(const abc_ctx* c, double t0, double t1) {
+  if (c->input_kind == ABC_INPUT_FENG) return feng_frame_integral(c->feng, t0, t1);
+  double s = 0.0, a = t0, va = pwl_at(c->kt, c->kc, t0);
+  for (size_t k = 0; k < c->kt.size(); ++k) {
+    if (c->kt[k] <= t0) continue;
+    if (c->kt[k] >= t1) break;
+    s += 0.5 * (c->kt[k] - a) * (va + c->kc[k]);
+    a = c->kt[k];
+    va = c->kc[k];
+  }
+  return s + 0.5 * (t1 - a) * (va + pwl_at(c->kt, c->kc, t1));
+}
+
+abc_status abc_patlak(abc_ctx* ctx, const float* tacs, uint64_t J, double t_star_min, uint32_t ptr_flags, float* ki,
+                      float* intercept) {
+  if (!ctx) return ABC_E_ARG;
+  if (!ctx->have_input || !ctx->have_frames) return fail(ctx, ABC_E_STATE, "input function and frames must be set");
+  if (ptr_flags & ~(ABC_PTR_TACS_DEVICE | ABC_PTR_OUT_DEVICE)) return fail(ctx, ABC_E_ARG, "unknown ptr_flags");
+  if (J == 0) return ABC_OK;
+  if (!tacs || !ki || !std::isfinite(t_star_min)) return fail(ctx, ABC_E_ARG, "bad Patlak arguments");
+  const uint32_t L = ctx->L;
+  // frame coefficients (draw- and voxel-independent): centred OLS as two dot products
+  std::vector<double> cp(L), x(L), ab(2 * L, 0.0);
+  uint32_t m = 0, f0 = L;
+  for (uint32_t f = 0; f < L; ++f) {
+    const double tm = ctx->fs[f] + 0.5 * ctx->fd[f];
+    cp[f] = input_integral_host(ctx, ctx->fs[f], ctx->fs[f] + ctx->fd[f]) / ctx->fd[f];
+    x[f] = input_integral_host(ctx, 0.0, tm) / cp[f];
+    if (tm >= t_star_min) {
+      ++m;
+      f0 = std::min(f0, f);
+    }
+  }
+  double xb = 0.0, sxx = 0.0;
+  for (uint32_t f = 0; f < L; ++f)
+    if (ctx->fs[f] + 0.5 * ctx->fd[f] >= t_star_min) xb += x[f];
+  xb = m ? xb / m : 0.0;
+  for (uint32_t f = 0; f < L; ++f)
+    if (ctx->fs[f] + 0.5 * ctx->fd[f] >= t_star_min) sxx += (x[f] - xb) * (x[f] - xb);
+  const bool valid = m >= 2 && sxx > 0.0;
+  for (uint32_t f = 0; f < L; ++f)
+    if (valid && ctx->fs[f] + 0.5 * ctx->fd[f] >= t_star_min) {
+      ab[f] = (x[f] - xb) / (sxx * cp[f]);
+      ab[L + f] = 1.0 / (double(m) * cp[f]);
+    }
+  CK(cudaSetDevice(ctx->dev));
+  const cudaStream_t st = ctx->stream;
+  CK(upload(ctx->pat_ab, ab));
+  const float* d_tacs = tacs;
+  if (!(ptr_flags & ABC_PTR_TACS_DEVICE)) {
+    CK(ctx->tacs.ensure(sizeof(float) * J * L));
+    CK(cudaMemcpyAsync(ctx->tacs.p, tacs, sizeof(float) * J * L, cudaMemcpyHostToDevice, st));
+    d_tacs = ctx->tacs.as<float>();
+  }
+  const bool dev_out = ptr_flags & ABC_PTR_OUT_DEVICE;
+  float* d_ki = ki;
+  float* d_ic = intercept;
+  if (!dev_out) {
+    CK(ctx->env_q.ensure(8 * J));
+    d_ki = ctx->env_q.as<float>();
+    d_ic = intercept ? d_ki + J : nullptr;
+  }
+  PatlakParams pp{d_tacs, J, L, f0 < L ? f0 : 0, ctx->pat_ab.as<double>(), ctx->pat_ab.as<double>() + L, xb,
+                  valid ? 1 : 0, d_ki, d_ic};
+  launch_patlak(pp, st);
+  CK(cudaGetLastError());
+  if (!dev_out) {
+    CK(cudaMemcpyAsync(ki, d_ki, 4 * J, cudaMemcpyDeviceToHost, st));
+    if (intercept) CK(cudaMemcpyAsync(intercept, d_ic, 4 * J, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  return ABC_OK;
+}
+
 abc_status abc_set_sim_noise(abc_ctx* ctx, double ell, double half_life_min) {
   if (!ctx) return ABC_E_ARG;
   if (!std::isfinite(ell) || ell < 0.0) return fail(ctx, ABC_E_ARG, "noise level must be finite and >= 0");
@@ -1061,7 +1138,7 @@ void abc_destroy(abc_ctx* ctx) {
                      &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob,
                      &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp, &ctx->item_log,
                      &ctx->dBt, &ctx->dS2, &ctx->dAt, &ctx->dY2,
-                     &ctx->env_idx, &ctx->env_t, &ctx->env_q, &ctx->proj};
+                     &ctx->env_idx, &ctx->env_t, &ctx->env_q, &ctx->proj, &ctx->pat_ab};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_finv, &ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,

@@ -352,6 +352,20 @@ struct EnvelopeParams {
 };
 void launch_response_envelope(const EnvelopeParams& p, cudaStream_t st);
 
+// Patlak K_i map (patlak.cu): abc_patlak.
+struct PatlakParams {
+  const float* tacs;   // [J][L]
+  uint64_t J;
+  uint32_t L, f0;      // frames f0.. carry the coefficients (the others are 0)
+  const double* a;     // [L] slope weights
+  const double* b;     // [L] mean-of-z weights
+  double xbar;
+  int valid;           // >= 2 late frames with spread in x
+  float* ki;           // [J]
+  float* intercept;    // [J] or nullptr
+};
+void launch_patlak(const PatlakParams& p, cudaStream_t st);
+
 struct EpsReduceParams {
   const double* mom;
   uint64_t J;
