@@ -263,9 +263,11 @@ __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* c
       double ss = 0.0;
       for (uint32_t a = lane; a < c; a += 32) ss += (sc[a] - mu) * (sc[a] - mu);
       ss = warp_sum(ss);
-      for (uint32_t a = c + lane; a < np2; a += 32) sc[a] = __longlong_as_double(0x7ff0000000000000ll);
+      uint32_t cp2 = 32;  // sort only the occupied power of two of this model's c values
+      while (cp2 < c) cp2 <<= 1;
+      for (uint32_t a = c + lane; a < cp2; a += 32) sc[a] = __longlong_as_double(0x7ff0000000000000ll);
       __syncwarp();
-      warp_sort_any(sc, nullptr, np2, lane);
+      warp_sort_any(sc, nullptr, cp2, lane);
       mean = float(mu);
       sd = c >= 2 ? float(sqrt(ss / double(c - 1))) : NANF;
       q3[0] = float(quantile7(sc, c, 0.025));
