@@ -347,23 +347,34 @@ __global__ void __launch_bounds__(32 * kPermWarps) permute_kernel(const OrderPar
       }
     }
     __syncwarp();
-    for (uint32_t k0 = 0; k0 < p.LP; k0 += 32) {
-      const uint32_t k = k0 + lane;
-      const bool on = k < p.LP;
-      const int src = on ? sperm[k] : -1;
-      const float ws = on ? swsp[k] : 0.0f;
-      float lo = 3.0e38f, hi = -3.0e38f;
-      for (uint32_t r = 0; r < nr; ++r) {
-        const float v = src >= 0 ? -__fmul_rn(ws, rows[r * stride + src]) : 0.0f;
-        if (on) p.bankp[(j0 + r) * p.LP + k] = v;
-        lo = fminf(lo, v);
-        hi = fmaxf(hi, v);
+    // the tile's nr x LP block of bankp is contiguous (LP % 4 == 0): 16-B stores, lane q writes
+    // frames 4(q % QP) .. +3 of row q / QP
+    const uint32_t QP = p.LP / 4;
+    float4* dst = reinterpret_cast<float4*>(p.bankp + j0 * p.LP);
+    for (uint32_t q = lane; q < nr * QP; q += 32) {
+      const float* row = rows + (q / QP) * stride;
+      const uint32_t k = 4 * (q % QP);
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int src = sperm[k + u];
+        v[u] = src >= 0 ? -__fmul_rn(swsp[k + u], row[src]) : 0.0f;
       }
-      if (on && p.tree && p.tbounds) {
+      dst[q] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    if (p.tree && p.tbounds)
+      for (uint32_t k = lane; k < p.LP; k += 32) {
+        const int src = sperm[k];
+        const float ws = swsp[k];
+        float lo = 3.0e38f, hi = -3.0e38f;
+        for (uint32_t r = 0; r < nr; ++r) {
+          const float v = src >= 0 ? -__fmul_rn(ws, rows[r * stride + src]) : 0.0f;
+          lo = fminf(lo, v);
+          hi = fmaxf(hi, v);
+        }
         p.tbounds[(t * 2 + 0) * p.LP + k] = lo;
         p.tbounds[(t * 2 + 1) * p.LP + k] = hi;
       }
-    }
     __syncwarp();
   }
 }
