@@ -17,7 +17,7 @@ namespace vpet {
 namespace {
 
 // ---- per-frame mean and spread of the prescaled bank over a strided sample ----
-__global__ void __launch_bounds__(256) frame_stats_kernel(const OrderParams p) {
+__global__ void __launch_bounds__(1024) frame_stats_kernel(const OrderParams p) {
   uint32_t f = blockIdx.x;
   uint64_t stride = p.N > 65536 ? p.N / 65536 : 1;
   uint64_t ns = (p.N + stride - 1) / stride;
@@ -28,46 +28,57 @@ __global__ void __launch_bounds__(256) frame_stats_kernel(const OrderParams p) {
     s1 += x;
     s2 += x * x;
   }
-  __shared__ double r1[256], r2[256];
-  r1[threadIdx.x] = s1;
-  r2[threadIdx.x] = s2;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      r1[threadIdx.x] += r1[threadIdx.x + o];
-      r2[threadIdx.x] += r2[threadIdx.x + o];
-    }
-    __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
-  if (threadIdx.x == 0) {
-    double m = r1[0] / double(ns);
-    p.var[f] = fmax(r2[0] / double(ns) - m * m, 0.0);
-    p.mean[f] = m;
+  __shared__ double r1[32], r2[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    r1[wid] = s1;
+    r2[wid] = s2;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = int(blockDim.x >> 5);
+    s1 = lane < nw ? r1[lane] : 0.0;
+    s2 = lane < nw ? r2[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      double m = s1 / double(ns);
+      p.var[f] = fmax(s2 / double(ns) - m * m, 0.0);
+      p.mean[f] = m;
+    }
   }
 }
 
-// ---- descending-spread permutation (stable), padded with -1 ----
-__global__ void frame_perm_kernel(const OrderParams p) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  int order[kMaxLP];
-  for (uint32_t f = 0; f < p.L; ++f) order[f] = int(f);
-  if (p.reorder) {
-    for (uint32_t a = 1; a < p.L; ++a) {
-      int x = order[a];
-      int b = int(a) - 1;
-      while (b >= 0 && p.var[order[b]] < p.var[x]) {
-        order[b + 1] = order[b];
-        --b;
+// ---- descending-spread permutation (stable), padded with -1: thread f places frame f at its
+// rank (frames of larger spread, or of equal spread and lower index, go first) ----
+__global__ void __launch_bounds__(kMaxLP) frame_perm_kernel(const OrderParams p) {
+  __shared__ int order[kMaxLP];
+  const uint32_t f = threadIdx.x;
+  if (f < p.L) {
+    uint32_t rank = f;
+    if (p.reorder) {
+      const double vf = p.var[f];
+      rank = 0;
+      for (uint32_t g = 0; g < p.L; ++g) {
+        const double vg = p.var[g];
+        rank += (vg > vf || (vg == vf && g < f)) ? 1u : 0u;
       }
-      order[b + 1] = x;
     }
+    order[rank] = int(f);
   }
-  for (uint32_t k = 0; k < p.LP; ++k) {
+  __syncthreads();
+  for (uint32_t k = f; k < p.LP; k += blockDim.x) {
     int src = k < p.L ? order[k] : -1;
     p.perm[k] = src;
     p.wsp[k] = src >= 0 ? p.wsc[src] : 0.0f;
   }
-  if (p.tree && p.pminmax)  // projection range accumulators (order-preserving uint of float)
+  if (f == 0 && p.tree && p.pminmax)  // projection range accumulators (order-preserving uint of float)
     for (int c = 0; c < kNPC; ++c) {
       p.pminmax[2 * c] = 0xffffffffu;
       p.pminmax[2 * c + 1] = 0u;
@@ -508,8 +519,8 @@ size_t order_sort_temp_bytes(uint64_t N) {
 }
 
 cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launches) {
-  frame_stats_kernel<<<p.L, 256, 0, st>>>(p);
-  frame_perm_kernel<<<1, 32, 0, st>>>(p);
+  frame_stats_kernel<<<p.L, 1024, 0, st>>>(p);
+  frame_perm_kernel<<<1, kMaxLP, 0, st>>>(p);
   *launches += 2;
   OrderParams q = p;
   if (p.tree) {
