@@ -93,6 +93,9 @@ typedef enum { ABC_INPUT_PWL = 0, ABC_INPUT_FENG = 1 } abc_input_kind;
                                     distance (y.s cross term on tcgen05, BF16x3 split; WL2, TOPN,
                                     L <= 48, else ABC_E_UNSUPPORTED).  Same certified results;
                                     evaluates every pair (SURVEY.md §8f-1, A/B comparison) */
+#define ABC_FLAG_FORCE_FALLBACK 0x80u /* test hook: certification rejects every voxel, so every
+                                    voxel is re-run by the exact FP64 scan (the uncertified-voxel
+                                    path of DESIGN.md §3); results must be unchanged */
 
 /* abc_run_voxels ptr_flags */
 #define ABC_PTR_TACS_DEVICE 0x1u /* tacs is a device pointer on ctx's device */
@@ -176,11 +179,15 @@ abc_status abc_set_frames(abc_ctx* ctx, const double* start_min, const double* d
                           const float* weight, uint32_t L);
 
 /* Run Alg. 1 for J voxels.  tacs: J x L FP32 row-major (frame-contiguous per voxel), host
- * or device per ptr_flags; negative values allowed, non-finite values -> ABC_E_ARG.
- * J = 0 is a no-op.  The work is ordered on the context's stream; the call returns after
- * the results are complete (host outputs) or enqueued (device outputs, see abc_sync).
+ * or device per ptr_flags; negative values allowed.  Non-finite values -> ABC_E_ARG: the
+ * kernels that follow the on-device finite check skip their work (the call returns in about
+ * the time of the bank stage) and the output arrays are left unspecified.
+ * J = 0 is a no-op.  The work is ordered on the context's stream (abc_set_stream); the call
+ * returns after the results are complete, for host and device outputs alike (it ends with a
+ * synchronisation of that stream, which also reads the status flags of the run).
  * ABC_E_NOMEM if the bank (2 x N x L FP32), the per-voxel state and the staging buffers
- * do not fit in free device memory (checked before allocating). */
+ * do not fit in free device memory (checked before allocating).  ABC_E_UNSUPPORTED if a
+ * kernel's shared-memory need exceeds the device's opt-in maximum. */
 abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t ptr_flags,
                           abc_result* out);
 

@@ -9,9 +9,9 @@
 
 The compute runs in libvpetabc.so (CUDA, sm_100a) through the C ABI in include/vpetabc.h.
 """
-from ._abi import (AbcError, FLAG_COUNT_WORK, FLAG_DENSE_TC, FLAG_EXACT, FLAG_NO_PRUNE, FLAG_NO_REORDER, FLAG_NO_TREE,  # noqa: F401
+from ._abi import (AbcError, FLAG_COUNT_WORK, FLAG_DENSE_TC, FLAG_EXACT, FLAG_FORCE_FALLBACK, FLAG_NO_PRUNE, FLAG_NO_REORDER, FLAG_NO_TREE,  # noqa: F401
                    FLAG_TIMING, load_library)
 from .context import AbcContext, family_width  # noqa: F401
 
 __all__ = ["AbcContext", "AbcError", "family_width", "load_library", "FLAG_TIMING", "FLAG_EXACT",
-           "FLAG_COUNT_WORK", "FLAG_DENSE_TC", "FLAG_NO_PRUNE", "FLAG_NO_REORDER", "FLAG_NO_TREE"]
+           "FLAG_COUNT_WORK", "FLAG_DENSE_TC", "FLAG_FORCE_FALLBACK", "FLAG_NO_PRUNE", "FLAG_NO_REORDER", "FLAG_NO_TREE"]

@@ -23,6 +23,7 @@ ACCEPTS = {"TOPN": 0, "EPS": 1}
 INPUTS = {"PWL": 0, "FENG": 1}
 FLAG_TIMING, FLAG_EXACT, FLAG_COUNT_WORK, FLAG_NO_PRUNE, FLAG_NO_REORDER, FLAG_NO_TREE = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 FLAG_DENSE_TC = 0x40
+FLAG_FORCE_FALLBACK = 0x80
 PTR_TACS_DEVICE, PTR_OUT_DEVICE = 0x1, 0x2
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_STATE", 3: "E_NOMEM", 4: "E_CUDA", 5: "E_UNSUPPORTED"}
 

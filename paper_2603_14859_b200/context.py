@@ -153,7 +153,26 @@ class AbcContext:
         return res
 
     def model_select(self, tacs):
-        return self.run_voxels(tacs, want=("prob", "preferred"))
+        """Model probabilities (J x M) and preferred model (J) through abc_model_select (P:109-114,
+        P:282).  numpy host array in -> numpy out; torch CUDA tensor in -> torch CUDA tensors out."""
+        if type(tacs).__module__.startswith("torch") and tacs.is_cuda:
+            import torch
+            if tacs.dtype != torch.float32 or not tacs.is_contiguous() or tacs.dim() != 2:
+                raise ValueError("tacs must be a contiguous 2-D float32 tensor")
+            J = int(tacs.shape[0])
+            prob = torch.empty((J, self.M), dtype=torch.float32, device=tacs.device)
+            pref = torch.empty(J, dtype=torch.int32, device=tacs.device)
+            self._check(self._lib.abc_model_select(self._h, C.c_void_p(tacs.data_ptr()) if J else None, J,
+                                                   A.PTR_TACS_DEVICE | A.PTR_OUT_DEVICE, C.c_void_p(prob.data_ptr()),
+                                                   C.c_void_p(pref.data_ptr())))
+            return {"prob": prob, "preferred": pref}
+        y = np.ascontiguousarray(tacs, dtype=np.float32)
+        J = y.shape[0]
+        prob = np.empty((J, self.M), dtype=np.float32)
+        pref = np.empty(J, dtype=np.int32)
+        self._check(self._lib.abc_model_select(self._h, A.host_ptr(y) if J else None, J, 0, prob.ctypes.data,
+                                               pref.ctypes.data))
+        return {"prob": prob, "preferred": pref}
 
     def patlak(self, tacs, t_star):
         """(K_i, intercept) per voxel: least-squares Patlak line over the frames with mid-time >=

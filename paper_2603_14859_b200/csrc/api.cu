@@ -18,6 +18,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -330,6 +332,25 @@ ErrBound dense_error_bound(uint32_t L) {
 }  // namespace
 
 namespace vpet {
+cudaError_t ensure_smem_attr(const void* func, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;  // (function, device) -> opted-in bytes
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{func, dev}];
+  if (have >= bytes) return cudaSuccess;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  if (bytes > size_t(optin)) return cudaErrorInvalidValue;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 // padded frame counts with a compiled FP32-pass instance (scan_kernels.cuh VPET_LP_LIST)
 static const uint32_t kLPs[] = {8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 56, 64, 80, 96, 128};
 bool scan_supported(uint32_t LP) {
@@ -797,6 +818,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     dp.heap = ctx->heap.as<unsigned long long>();
     dp.heap_cnt = ctx->heap_cnt.as<uint32_t>();
     dp.tau_glob = ctx->tau_glob.as<unsigned int>();
+    dp.bad = ctx->flag.as<int>();
     launch_fill_u32(ctx->tau_glob.as<uint32_t>(), 0x7f800000u, J, st);
     ++launches;
     CK(launch_dense(dp, ctx->bank.as<float>(), LS, d_tacs, ctx->d_wsc.as<float>(), st, &launches));
@@ -825,6 +847,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     sp.eb = eb;
     sp.prior_g = ctx->d_prior.as<PriorDev>();
     sp.M = M;
+    sp.bad = ctx->flag.as<int>();
     if (tree) {
       sp.idxmap = ctx->idxmap.as<uint32_t>();
       sp.tbounds = ctx->tbounds.as<float>();
@@ -890,6 +913,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   rp.P = P;
   rp.fb_list = ctx->fb_list.as<uint32_t>();
   rp.fb_len = ctx->fb_len.as<uint32_t>();
+  rp.force_fb = (ctx->cfg.flags & ABC_FLAG_FORCE_FALLBACK) ? 1 : 0;
+  rp.bad = ctx->flag.as<int>();
   rp.out = dout;
 
   ExactParams xp{};
@@ -904,6 +929,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   xp.J = J;
   xp.hd = ctx->hd.as<double>();
   xp.hi = ctx->hidx.as<uint32_t>();
+  xp.bad = ctx->flag.as<int>();
 
   if (eps) {
     EpsReduceParams ep{ctx->mom.as<double>(), J, ctx->prior, P, dout};
@@ -917,14 +943,14 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     rp.list = nullptr;
     rp.list_len = nullptr;
     rec(EV_CERT);
-    launch_certify_reduce(rp, st);
+    CK(launch_certify_reduce(rp, st));
     launches += 2;
     rec(EV_FB);
   } else {
     rp.exact = 0;
     rp.list = nullptr;
     rp.list_len = nullptr;
-    launch_certify_reduce(rp, st);
+    CK(launch_certify_reduce(rp, st));
     ++launches;
     rec(EV_CERT);
     // uncertified voxels: exact scan + reduce over the device-side list (no host sync)
@@ -936,7 +962,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     rx.list = xp.list;
     rx.list_len = xp.list_len;
     rx.fb_list = nullptr;
-    launch_certify_reduce(rx, st);
+    rx.force_fb = 0;
+    CK(launch_certify_reduce(rx, st));
     launches += 2;
     rec(EV_FB);
   }
@@ -1106,8 +1133,7 @@ abc_status abc_response_envelope(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t
   CK(ctx->flag.ensure(16));
   CK(cudaMemsetAsync(ctx->flag.p, 0, 16, st));
   EnvelopeParams ep{d_idx, J, ctx->N, n_acc, T, ctx->env_t.as<double>(), ctx->prior, d_q, ctx->flag.as<int>()};
-  launch_response_envelope(ep, st);
-  CK(cudaGetLastError());
+  CK(launch_response_envelope(ep, st));
   if (!dev_out) CK(cudaMemcpyAsync(q, d_q, 12 * J * T, cudaMemcpyDeviceToHost, st));
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, ctx->flag.p, 4, cudaMemcpyDeviceToHost, st));

@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
   double* cd = reinterpret_cast<double*>(smem_raw + per_warp * w);
   double* sc = cd + Kp;
   uint32_t* ci = reinterpret_cast<uint32_t*>(sc + np2);
+  if (p.bad && *p.bad) return;  // non-finite TACs: no results (ABC_E_ARG)
   const uint64_t len = p.list_len ? uint64_t(*p.list_len) : p.J;
   const uint64_t nwarps = uint64_t(gridDim.x) * wpc;
   const double DINF = __longlong_as_double(0x7ff0000000000000ll);
@@ -330,6 +331,10 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
         B = tmax;
+      }
+      if (p.force_fb) {  // ABC_FLAG_FORCE_FALLBACK: every voxel takes the exact path (test hook)
+        if (lane == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+        continue;
       }
       const bool complete = (total == p.N);  // every draw was kept: nothing excluded
       if (!complete && !(B < __int_as_float(0x7f800000))) {  // no finite bound (non-finite D32s)
@@ -430,27 +435,57 @@ __device__ __noinline__ double exact_push(double* hd, uint32_t* hi, uint32_t n, 
   return cnt >= n ? hd[0] : __longlong_as_double(0x7ff0000000000000ll);
 }
 
-__global__ void __launch_bounds__(64) exact_scan_kernel(const ExactParams p) {
+// Warp per voxel: lane l scores draws l, l + 32, ... in FP64 (operation for operation as the
+// oracle), with prefix pruning against the warp-uniform threshold tau (the n-th smallest (D, i) so
+// far: prefix sums of non-negative terms only grow, so a prefix >= tau means D >= tau).  Survivors
+// are pushed by their own lane, one lane at a time in lane order, into the voxel's max-heap of the
+// n smallest (D64, i); the new root is then broadcast.  The heap holds exactly the n smallest keys
+// of the draws seen, so the result does not depend on the interleaving.
+__global__ void __launch_bounds__(256) exact_scan_kernel(const ExactParams p) {
+  if (p.bad && *p.bad) return;  // non-finite TACs: no results (ABC_E_ARG)
+  const int lane = threadIdx.x & 31;
   const uint64_t len = p.list_len ? uint64_t(*p.list_len) : p.J;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < len; e += stride) {
+  const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+  const double DINF = __longlong_as_double(0x7ff0000000000000ll);
+  for (uint64_t e = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; e < len; e += nwarps) {
     const uint64_t v = p.list ? p.list[e] : e;
     const float* y = p.tacs + v * p.L;
     double* hd = p.hd + v * p.n;
     uint32_t* hi = p.hi + v * p.n;
-    uint32_t cnt = 0;
-    double tau = __longlong_as_double(0x7ff0000000000000ll);
-    for (uint64_t i = 0; i < p.N; ++i) {
-      const float* s = p.bank + i * p.LS;
-      double D = 0.0;
-      bool rej = false;
-      for (uint32_t f = 0; f < p.L; ++f) {
-        double d = __dsub_rn(double(__ldg(y + f)), double(__ldg(s + f)));
-        double t = (p.dist == ABC_DIST_L1) ? fabs(d) : __dmul_rn(d, d);
-        D = __dadd_rn(D, __dmul_rn(double(__ldg(p.w + f)), t));
-        if (D >= tau) { rej = true; break; }  // prefix sums are monotone: D_final >= tau
+    uint32_t cnt = 0;  // warp-uniform
+    double tau = DINF;
+    uint32_t tau_i = 0xffffffffu;  // index of the root: keys compare as (D, i)
+    for (uint64_t base = 0; base < p.N; base += 32) {
+      const uint64_t i = base + lane;
+      double D = DINF;
+      bool cand = false;
+      if (i < p.N) {
+        const float* s = p.bank + i * p.LS;
+        D = 0.0;
+        bool rej = false;
+        for (uint32_t f = 0; f < p.L; ++f) {
+          double d = __dsub_rn(double(__ldg(y + f)), double(__ldg(s + f)));
+          double t = (p.dist == ABC_DIST_L1) ? fabs(d) : __dmul_rn(d, d);
+          D = __dadd_rn(D, __dmul_rn(double(__ldg(p.w + f)), t));
+          if (D > tau) { rej = true; break; }  // prefix > tau => D > tau (D == tau decided by index)
+        }
+        cand = !rej && (cnt < p.n || pair_gt(tau, tau_i, D, uint32_t(i)));
       }
-      if (!rej && D < tau) tau = exact_push(hd, hi, p.n, cnt, D, uint32_t(i));
+      uint32_t bal = __ballot_sync(0xffffffffu, cand);
+      while (bal) {
+        const int src = __ffs(bal) - 1;
+        bal &= bal - 1;
+        if (lane == src && (cnt < p.n || pair_gt(tau, tau_i, D, uint32_t(i)))) {
+          exact_push(hd, hi, p.n, cnt, D, uint32_t(i));
+        }
+        __syncwarp();
+        cnt = __shfl_sync(0xffffffffu, cnt, src);
+        if (cnt >= p.n) {
+          tau = hd[0];
+          tau_i = hi[0];
+        }
+        __syncwarp();
+      }
     }
   }
 }
@@ -585,7 +620,7 @@ __global__ void response_envelope_kernel(const EnvelopeParams p, uint32_t np2, u
 
 }  // namespace
 
-void launch_certify_reduce(const ReduceParams& p, cudaStream_t st) {
+cudaError_t launch_certify_reduce(const ReduceParams& p, cudaStream_t st) {
   uint32_t Kp = next_pow2(p.exact ? p.n : (p.K * p.nparts > p.n ? p.K * p.nparts : p.n));
   if (Kp < 32) Kp = 32;
   uint32_t np2 = next_pow2(p.n);
@@ -594,23 +629,21 @@ void launch_certify_reduce(const ReduceParams& p, cudaStream_t st) {
   uint32_t wpc = 8;
   while (wpc > 1 && per_warp * wpc > 96 * 1024) wpc >>= 1;
   size_t smem = per_warp * wpc;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(certify_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = smem;
-  }
+  cudaError_t e = ensure_smem_attr((const void*)certify_reduce_kernel, smem);
+  if (e != cudaSuccess) return e;
   uint64_t work = p.list ? p.J : p.J;  // upper bound on list length
   uint64_t blocks = (work + wpc - 1) / wpc;
   if (blocks > 148ull * 64) blocks = 148ull * 64;
   if (blocks == 0) blocks = 1;
   certify_reduce_kernel<<<unsigned(blocks), wpc * 32, smem, st>>>(p, Kp, np2, wpc);
+  return cudaGetLastError();
 }
 
 void launch_exact_scan(const ExactParams& p, cudaStream_t st) {
-  uint64_t blocks = (p.J + 63) / 64;
+  uint64_t blocks = (p.J + 7) / 8;  // 8 warps per CTA, one voxel per warp
   if (blocks > 148ull * 8) blocks = 148ull * 8;
   if (blocks == 0) blocks = 1;
-  exact_scan_kernel<<<unsigned(blocks), 64, 0, st>>>(p);
+  exact_scan_kernel<<<unsigned(blocks), 256, 0, st>>>(p);
 }
 
 void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st) {
@@ -619,22 +652,20 @@ void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st) {
   eps_reduce_kernel<<<unsigned(blocks), 128, 0, st>>>(p);
 }
 
-void launch_response_envelope(const EnvelopeParams& p, cudaStream_t st) {
+cudaError_t launch_response_envelope(const EnvelopeParams& p, cudaStream_t st) {
   uint32_t np2 = next_pow2(p.n_acc);
   if (np2 < 32) np2 = 32;
   const size_t per_warp = size_t(np2) * 28;
   uint32_t wpc = 8;
   while (wpc > 1 && per_warp * wpc > 96 * 1024) wpc >>= 1;
   const size_t smem = per_warp * wpc;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(response_envelope_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = smem;
-  }
+  cudaError_t e = ensure_smem_attr((const void*)response_envelope_kernel, smem);
+  if (e != cudaSuccess) return e;
   uint64_t blocks = (p.J + wpc - 1) / wpc;
   if (blocks > 148ull * 32) blocks = 148ull * 32;
   if (blocks == 0) blocks = 1;
   response_envelope_kernel<<<unsigned(blocks), wpc * 32, smem, st>>>(p, np2, wpc);
+  return cudaGetLastError();
 }
 
 }  // namespace vpet

@@ -275,6 +275,7 @@ struct ScanParams {
   unsigned int* queue;      // work-queue counter (zeroed per run)
   unsigned long long* item_log;  // diagnostics (env VPET_ITEMLOG): [item][4] = start ns, end ns, SM, voxel tile
   const uint32_t* vorder;   // [J] voxel processed in slot j (tree mode) or nullptr (identity)
+  const int* bad;           // set by the finite check when a TAC value is not finite: skip all work
 };
 // Candidate heaps: 8-ary max-heaps; node i lives at slot i + kHeapOff of a (voxel, part) row of
 // heap_stride(K) keys, so the 8 children of node i (slots 8i + 8 .. 8i + 15) are one 64-B group.
@@ -304,6 +305,7 @@ struct ExactParams {
   uint64_t J;
   double* hd;         // [J][n] exact heap distances
   uint32_t* hi;       // [J][n] exact heap indices
+  const int* bad;     // non-finite TACs: skip all work
 };
 void launch_exact_scan(const ExactParams& p, cudaStream_t st);
 
@@ -335,10 +337,12 @@ struct ReduceParams {
   // fallback output
   uint32_t* fb_list;
   uint32_t* fb_len;
+  int force_fb;       // ABC_FLAG_FORCE_FALLBACK: send every voxel to the exact scan (test hook)
+  const int* bad;     // non-finite TACs: skip all work
   // results (device pointers, may be null)
   abc_result out;
 };
-void launch_certify_reduce(const ReduceParams& p, cudaStream_t st);
+cudaError_t launch_certify_reduce(const ReduceParams& p, cudaStream_t st);
 
 // Response-function envelope (Fig. 1): abc_response_envelope.
 struct EnvelopeParams {
@@ -350,7 +354,7 @@ struct EnvelopeParams {
   float* q;                 // [J][T][3]
   int* bad;                 // set when an index is >= N
 };
-void launch_response_envelope(const EnvelopeParams& p, cudaStream_t st);
+cudaError_t launch_response_envelope(const EnvelopeParams& p, cudaStream_t st);
 
 // Patlak K_i map (patlak.cu): abc_patlak.
 struct PatlakParams {
@@ -376,6 +380,10 @@ struct EpsReduceParams {
 void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st);
 
 void launch_fill_u32(uint32_t* p, uint32_t v, uint64_t n, cudaStream_t st);
+// Opt `func` in to `bytes` of dynamic shared memory on the CURRENT device (the attribute is per
+// device; cached per (function, device), thread-safe).  Returns the CUDA error of the opt-in, or
+// cudaErrorInvalidValue when `bytes` exceeds the device's opt-in maximum.
+cudaError_t ensure_smem_attr(const void* func, size_t bytes);
 
 // K6 (dense_tc.cu): shared-bank tensor-core distance, ABC_FLAG_DENSE_TC (WL2, top-n, L <= 48).
 // Operands live in HBM pre-tiled in the UMMA no-swizzle K-major core-matrix layout (bf16 bits).
@@ -389,6 +397,7 @@ struct DenseParams {
   unsigned long long* heap;  // [J][2][heap_stride(K)]: part = column half of each draw tile
   uint32_t* heap_cnt;        // [J][2]
   unsigned int* tau_glob;    // [J]
+  const int* bad;            // non-finite TACs: skip all work
 };
 uint64_t dense_bank_bytes(uint64_t N);
 uint64_t dense_voxel_bytes(uint64_t J);

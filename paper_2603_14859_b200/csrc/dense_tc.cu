@@ -149,6 +149,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 // ---- main kernel -------------------------------------------------------------------------------
 __global__ void __launch_bounds__(NTH, 1) dense_tc_kernel(const DenseParams p) {
+  if (p.bad && *p.bad) return;  // non-finite TACs: the call fails with ABC_E_ARG
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* sA = smem;
   unsigned char* sB = smem + A_BYTES;  // [2][B_BYTES]
@@ -313,11 +314,9 @@ cudaError_t launch_dense(DenseParams p, const float* bank, uint32_t LS, const fl
       bank, p.N, Npad, p.L, LS, wsc, p.Bt, p.S2);
   prep_voxel_kernel<<<unsigned(std::min<uint64_t>((Jpad + 255) / 256, 148 * 16)), 256, 0, st>>>(
       tacs, p.J, Jpad, p.L, wsc, p.At, p.Y2);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dense_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM));
+  {
+    cudaError_t e = ensure_smem_attr((const void*)dense_tc_kernel, SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   dense_tc_kernel<<<unsigned(Jpad / BM), NTH, SMEM, st>>>(p);
   if (launches) *launches += 3;

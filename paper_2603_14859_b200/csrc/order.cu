@@ -544,11 +544,8 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
   }
   {
     const size_t psmem = sizeof(float) * kPermWarps * kTile * (p.LS + 1);
-    static size_t attr = 0;
-    if (psmem > 48 * 1024 && psmem > attr) {
-      cudaFuncSetAttribute(permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(psmem));
-      attr = psmem;
-    }
+    cudaError_t ea = ensure_smem_attr((const void*)permute_kernel, psmem);
+    if (ea != cudaSuccess) return ea;
     permute_kernel<<<148 * 8, 32 * kPermWarps, psmem, st>>>(q);
     *launches += 1;
   }

@@ -546,6 +546,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_flat_kernel(const Sc
   float* stage = reinterpret_cast<float*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NST * (Shape<LP>::STAGE_FLOATS * 4 + T * 4));
   int* arrivals = reinterpret_cast<int*>(full + NST);
+  if (p.bad && *p.bad) return;  // non-finite TACs: the call fails with ABC_E_ARG, skip the work
   const int tid = threadIdx.x, lane = tid & 31;
   const uint64_t N = p.N;
   const uint32_t ntile = uint32_t((N + T - 1) / T);
@@ -709,6 +710,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
   unsigned long long* htop_t = VPET_SHEAP ? htop + threadIdx.x * 9 : nullptr;
   const uint32_t htop_s = smem_u32(htop) + uint32_t(threadIdx.x) * 72u;  // this thread's heap tops (bytes)
 
+  if (p.bad && *p.bad) return;  // non-finite TACs: the call fails with ABC_E_ARG, skip the work
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t N = p.N;
   const float* __restrict__ bankp = p.bankp;
@@ -933,11 +935,9 @@ template <int LP, int DIST, bool COUNT, bool TREE>
 cudaError_t launch_one(const ScanParams& p, cudaStream_t st) {
   using S = Shape<LP>;
   auto kern = TREE ? scan_tree_kernel<LP, DIST, COUNT> : scan_flat_kernel<LP, DIST, COUNT>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
+  {
+    cudaError_t e = ensure_smem_attr((const void*)kern, S::SMEM);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   uint64_t per_cta = uint64_t(NT) * S::R;
   uint64_t nvt = (p.J + per_cta - 1) / per_cta;

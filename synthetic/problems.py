@@ -182,6 +182,14 @@ def noise_fdg(C, start, dur, ell, half_life, rng):
     return C + ell * sig * rng.standard_normal(C.shape)
 
 
+def noise_fdg_eps(C, start, dur, ell, half_life, eps):
+    """noise_fdg with the standard normals `eps` given (same shape as C)."""
+    lam = math.log(2.0) / half_life
+    mid = np.asarray(start) + 0.5 * np.asarray(dur)
+    sig = np.sqrt(np.maximum(C, 0.0) * np.exp(-lam * mid) / dur) * np.exp(lam * mid)
+    return C + ell * sig * eps
+
+
 def noise_rt_gauss(C, start, dur, ell1, half_life, rng):
     """epsilon ~ N(0, ell1 sqrt(C / (dt e^{lam t})))  (Gaussian variant)."""
     lam = math.log(2.0) / half_life
@@ -314,9 +322,12 @@ def tb_voxel_count():
 
 
 def config4_chunk(chunk=0, n_chunks=32, N=10_000_000, n=18, seed=1004, abc_seed=2026, device="cpu",
-                  max_voxels=None, distance="WL2"):
+                  max_voxels=None, distance="WL2", voxel_index=None):
     """Axial slices z = chunk, chunk + n_chunks, ... of the TB phantom (raster order within each
-    slice).  IDIF = frame means of the Feng curve + 2 % noise as PWL knots."""
+    slice; n_chunks = 1 is the whole 4,441,800-voxel volume).  IDIF = frame means of the Feng
+    curve + 2 % noise as PWL knots.  voxel_index selects voxels of the chunk (e.g. a
+    stratified sample) before the ground truth is integrated; the TACs of a voxel do not depend on
+    which other voxels are generated."""
     start, dur = tb35()
     lo, hi = priors_fdg()
     feng = FENG_PHANTOM
@@ -334,15 +345,23 @@ def config4_chunk(chunk=0, n_chunks=32, N=10_000_000, n=18, seed=1004, abc_seed=
     theta = np.concatenate(thetas)
     lab = np.concatenate(labels)
     zz = np.concatenate(zs)
+    pos = np.concatenate([np.arange(len(t)) for t in thetas])  # position within the slice
     if max_voxels is not None:
-        theta, lab, zz = theta[:max_voxels], lab[:max_voxels], zz[:max_voxels]
+        theta, lab, zz, pos = theta[:max_voxels], lab[:max_voxels], zz[:max_voxels], pos[:max_voxels]
+    if voxel_index is not None:
+        vi = np.asarray(voxel_index)
+        theta, lab, zz, pos = theta[vi], lab[vi], zz[vi], pos[vi]
     C = truth_2tcm(theta, feng, start, dur, device)
-    ys = []
+    y = np.empty(C.shape, dtype=np.float32)
+    order = np.argsort(zz, kind="stable")
+    zs_sorted = zz[order]
     for z in np.unique(zz):
-        sel = zz == z
+        a, b = np.searchsorted(zs_sorted, [z, z + 1])
+        sel = order[a:b]
         rng = np.random.default_rng([seed, int(z), 1])
-        ys.append(noise_fdg(C[sel], start, dur, 7.0, T_HALF_F18, rng))
-    y = np.concatenate(ys).astype(np.float32)
+        nz = len(tb_geometry(int(z))[0])
+        eps = rng.standard_normal((nz, C.shape[1]))[pos[sel]]  # the slice's noise field, same for any subset
+        y[sel] = noise_fdg_eps(C[sel], start, dur, 7.0, T_HALF_F18, eps)
     idif_rng = np.random.default_rng([seed, 999_999])
     fm = feng_frame_means(feng, start, dur)
     fm = fm * (1.0 + 0.02 * idif_rng.standard_normal(fm.shape))

@@ -68,6 +68,12 @@ def compare(gpu: dict, ora: dict, topn: bool = True, max_exempt_frac: float = 0.
                 continue
             same[j] = False
             exempt += 1
+            # a voxel whose accepted set differs only by boundary swaps still obeys
+            # |P_gpu(m) - P_oracle(m)| <= (#swaps)/n and |count_gpu - count_oracle| <= #swaps
+            swaps = len(sg - so)
+            n = gi.shape[1]
+            assert np.all(np.abs(gpu["count"][j].astype(np.int64) - ora["count"][j].astype(np.int64)) <= swaps), j
+            assert np.all(np.abs(gpu["prob"][j].astype(np.float64) - ora["prob"][j]) <= swaps / n + PROB_ATOL), j
         assert exempt <= max(1, max_exempt_frac * J), f"{exempt} of {J} voxels differ at the boundary"
     else:
         same = np.all(gpu["count"] == ora["count"], axis=1)

@@ -8,7 +8,17 @@ import numpy as np
 import pytest
 import torch.multiprocessing as mp
 
-from paper_2603_14859_b200.distributed import shard_range
+from paper_2603_14859_b200.distributed import shard_indices, shard_range, shard_size
+
+
+def test_shard_indices_interleaved_partition():
+    for J in (0, 1, 7, 64, 1001):
+        for world in (1, 2, 3, 8):
+            parts = [shard_indices(J, world, r) for r in range(world)]
+            assert sorted(np.concatenate(parts).tolist()) == list(range(J))
+            assert [len(p) for p in parts] == [shard_size(J, world, r) for r in range(world)]
+            assert max(map(len, parts)) - min(map(len, parts)) <= 1
+            assert shard_size(J, world, 0) == max(map(len, parts))
 
 
 def test_shard_range_balanced_and_covering():

@@ -209,3 +209,86 @@ def test_device_pointers_and_stream(tb_small):
         if b.dtype == np.uint32:
             a = a.astype(np.uint32)
         np.testing.assert_array_equal(np.nan_to_num(a), np.nan_to_num(b), err_msg=k)
+
+
+def test_forced_fallback_equals_oracle_and_default(tb_small):
+    """ABC_FLAG_FORCE_FALLBACK sends every voxel through the uncertified-voxel path (the on-device
+    list, the warp-parallel exact FP64 scan and the exact reduction): same results as the oracle
+    and bit-identical to the certified FP32 path."""
+    from paper_2603_14859_b200 import FLAG_FORCE_FALLBACK, FLAG_TIMING
+    sub = tb_small.subset(np.arange(160))
+    base, _ = run_gpu(sub)
+    fb, ctx = run_gpu(sub, flags=FLAG_FORCE_FALLBACK | FLAG_TIMING)
+    assert ctx.stats()["n_fallback"] == sub.J
+    for k in base:
+        np.testing.assert_array_equal(np.nan_to_num(base[k]), np.nan_to_num(fb[k]), err_msg=k)
+    o, _ = run_oracle(sub)
+    compare(fb, o)
+
+
+def test_exact_ties_fixed_parameter_prior(tb_small):
+    """Exact D ties: model 0 has a fixed-parameter prior (lo == hi), so its whole
+    block of draws simulates the same TAC; ties are resolved towards the lower draw index.  The
+    fixed value is the truth of voxel 0, so the tied block fills voxel 0's accepted set."""
+    th = tb_small.truth["theta"][0].astype(np.float32)
+    lo, hi = S.priors_fdg()
+    fixed = [float(v) for v in th]
+    fixed[3] = 0.0
+    models = [dict(kind="2TCM_IRR", n_draws=3000, lo=fixed, hi=fixed),
+              dict(kind="2TCM_REV", n_draws=5000, lo=lo, hi=hi)]
+    p = tb_small.replace(models=models).subset(np.arange(64))
+    g, _ = run_gpu(p)
+    o, _ = run_oracle(p)
+    compare(g, o)
+    # voxel 0: the oracle accepts the 18 lowest indices of the tied block; the GPU must pick the same
+    # ones (compare() alone would allow swaps among draws tied exactly at the boundary)
+    assert np.array_equal(o["acc_idx"][0], np.arange(18, dtype=np.uint64))
+    assert np.array_equal(g["acc_idx"][0], o["acc_idx"][0])
+    # every draw identical: the first n indices, D equal
+    allfix = p.replace(models=[dict(kind="2TCM_IRR", n_draws=1000, lo=fixed, hi=fixed)], n_accept=7)
+    g2, _ = run_gpu(allfix)
+    o2, _ = run_oracle(allfix)
+    assert np.array_equal(g2["acc_idx"], np.tile(np.arange(7, dtype=np.uint64), (p.J, 1)))
+    compare(g2, o2)
+
+
+def test_model_select_entry_point(tb_small):
+    """abc_model_select (the north star's model-selection call) through the C ABI, host and device."""
+    import torch
+    from paper_2603_14859_b200 import AbcContext
+    ctx = AbcContext(**tb_small.ctx_kwargs)
+    tb_small.setup(ctx)
+    full = ctx.run_voxels(tb_small.tacs)
+    ms = ctx.model_select(tb_small.tacs)
+    np.testing.assert_array_equal(ms["prob"], full["prob"])
+    np.testing.assert_array_equal(ms["preferred"], full["preferred"])
+    md = ctx.model_select(torch.from_numpy(tb_small.tacs).cuda())
+    np.testing.assert_array_equal(md["prob"].cpu().numpy(), full["prob"])
+    np.testing.assert_array_equal(md["preferred"].cpu().numpy(), full["preferred"])
+    o, _ = run_oracle(tb_small)
+    np.testing.assert_allclose(ms["prob"], o["prob"], atol=1e-3 + 1.0 / 18)
+
+
+def test_nonfinite_voxel_returns_quickly(tb_small):
+    """A NaN TAC value gives ABC_E_ARG without the work of an unprunable voxel (the kernels after
+    the on-device finite check skip their work)."""
+    import time
+    from paper_2603_14859_b200 import AbcContext, AbcError
+    models = [dict(m, n_draws=1_000_000) for m in tb_small.ctx_kwargs["models"]]
+    p = tb_small.replace(models=models)
+    ctx = AbcContext(**p.ctx_kwargs)
+    p.setup(ctx)
+    ctx.run_voxels(p.tacs)  # warm: buffers allocated
+    t = time.perf_counter()
+    ctx.run_voxels(p.tacs)
+    t_ok = time.perf_counter() - t
+    bad = p.tacs.copy()
+    bad[5, 3] = np.nan
+    t = time.perf_counter()
+    with pytest.raises(AbcError) as e:
+        ctx.run_voxels(bad)
+    t_bad = time.perf_counter() - t
+    assert e.value.status == 1
+    assert t_bad < max(2.0 * t_ok, 0.2), (t_bad, t_ok)
+    r = ctx.run_voxels(p.tacs)  # the context stays usable
+    assert np.all(np.isfinite(r["ki_mean"]))
