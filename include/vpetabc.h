@@ -246,6 +246,19 @@ abc_status abc_set_sim_noise(abc_ctx* ctx, double ell, double half_life_min);
 abc_status abc_response_envelope(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc,
                                  const double* t_min, uint32_t T, uint32_t ptr_flags, float* q);
 
+/* Posterior summaries of given accepted lists (the reduction step of P:177-180, P:282 alone;
+ * SURVEY.md §8f-3).  For voxel j the first n_use entries of row j of acc_idx (J x n_acc draw
+ * indices, row-major) are reduced exactly as abc_run_voxels reduces its accepted set: counts,
+ * probabilities, preferred model, conditional mean / SD / type-7 quantiles, K_i.  A top-n row of
+ * abc_run_voxels is sorted by (D, index), so its prefix of length n' IS the top-n' accepted set of
+ * the same run: one run at the largest n gives every smaller n of a pilot sweep.
+ * acc_idx: host, or device with ABC_PTR_TACS_DEVICE.  out: as for abc_run_voxels (host, or device
+ * with ABC_PTR_OUT_DEVICE); out->acc_idx (J x n_use) receives the prefix; out->acc_dist must be
+ * NULL.  Needs only abc_init (the prior).  ABC_E_ARG: n_use == 0, n_use > n_acc, n_use > 4096,
+ * acc_dist != NULL, or an index >= N (detected on device after the work).  Blocks until done. */
+abc_status abc_reduce_accepted(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc, uint32_t n_use,
+                               uint32_t ptr_flags, abc_result* out);
+
 const char* abc_last_error(const abc_ctx* ctx);
 void abc_destroy(abc_ctx* ctx);
 uint32_t abc_abi_version(void);

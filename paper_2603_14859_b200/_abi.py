@@ -30,7 +30,7 @@ STATUS = {0: "OK", 1: "E_ARG", 2: "E_STATE", 3: "E_NOMEM", 4: "E_CUDA", 5: "E_UN
 SYMBOLS = ("abc_init", "abc_set_input_function", "abc_set_frames", "abc_run_voxels", "abc_model_select",
            "abc_set_stream", "abc_sync", "abc_get_stats", "abc_get_bank", "abc_last_error", "abc_destroy",
            "abc_abi_version", "abc_response_envelope",
-           "abc_set_sim_noise", "abc_patlak")
+           "abc_set_sim_noise", "abc_patlak", "abc_reduce_accepted")
 
 
 class ModelSpec(C.Structure):
@@ -92,6 +92,7 @@ def load_library(path: str = LIB_PATH):
     L.abc_set_sim_noise.argtypes = [vp, C.c_double, C.c_double]
     L.abc_patlak.argtypes = [vp, vp, C.c_uint64, C.c_double, C.c_uint32, vp, vp]
     L.abc_response_envelope.argtypes = [vp, vp, C.c_uint64, C.c_uint32, vp, C.c_uint32, C.c_uint32, vp]
+    L.abc_reduce_accepted.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(Result)]
     L.abc_set_stream.argtypes = [vp, vp]
     L.abc_sync.argtypes = [vp]
     L.abc_get_stats.argtypes = [vp, C.POINTER(Stats)]

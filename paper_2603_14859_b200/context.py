@@ -152,6 +152,41 @@ class AbcContext:
         self._check(self._lib.abc_run_voxels(self._h, tptr, J, flags, C.byref(r)))
         return res
 
+    def reduce_accepted(self, acc_idx, n_use, want=("prob", "preferred", "count", "mean", "sd", "q", "ki_mean",
+                                                    "ki_sd", "ki_q")):
+        """Posterior summaries of the first n_use accepted draws of each row of acc_idx (J x n_acc)
+        through abc_reduce_accepted: for a sorted top-n list this is the top-n_use result of the same
+        run (SURVEY §8f-3 pilot sweep by truncation).  numpy in -> numpy out; torch CUDA in -> torch
+        CUDA out."""
+        shapes = self.shapes(0)
+        if type(acc_idx).__module__.startswith("torch") and acc_idx.is_cuda:
+            import torch
+            idx = acc_idx.to(torch.int64).contiguous()
+            J, n_acc = int(idx.shape[0]), int(idx.shape[1])
+            tdt = {np.float32: torch.float32, np.int32: torch.int32, np.uint32: torch.int32, np.uint64: torch.int64}
+            res = {}
+            for name in want:
+                shp = (J, int(n_use)) if name == "acc_idx" else (J,) + shapes[name][1:]
+                res[name] = torch.empty(shp, dtype=tdt[_DTYPES[name]], device=idx.device)
+            r = A.Result()
+            for name, arr in res.items():
+                setattr(r, name, arr.data_ptr())
+            self._check(self._lib.abc_reduce_accepted(self._h, C.c_void_p(idx.data_ptr()), J, n_acc, int(n_use),
+                                                      A.PTR_TACS_DEVICE | A.PTR_OUT_DEVICE, C.byref(r)))
+            return res
+        idx = np.ascontiguousarray(acc_idx, dtype=np.uint64)
+        J, n_acc = idx.shape
+        res = {}
+        for name in want:
+            shp = (J, int(n_use)) if name == "acc_idx" else (J,) + shapes[name][1:]
+            res[name] = np.empty(shp, dtype=_DTYPES[name])
+        r = A.Result()
+        for name, arr in res.items():
+            setattr(r, name, arr.ctypes.data)
+        self._check(self._lib.abc_reduce_accepted(self._h, idx.ctypes.data if J else None, J, n_acc, int(n_use), 0,
+                                                  C.byref(r)))
+        return res
+
     def model_select(self, tacs):
         """Model probabilities (J x M) and preferred model (J) through abc_model_select (P:109-114,
         P:282).  numpy host array in -> numpy out; torch CUDA tensor in -> torch CUDA tensors out."""

@@ -614,7 +614,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (tree) need += 24 * J + vsort_tmp;
   if (!eps) need += (size_t(8) * heap_stride(std::max<uint32_t>(K, 1)) + 4) * J * nparts + 4 * J;  // heaps
   need += size_t(12) * J * (n ? n : 1);                  // exact heaps (fallback)
-  if (eps) need += sizeof(double) * J * M * MOMW;
+  if (eps) need += sizeof(Fix128) * J * nparts * M * MOMW;
   if (host_tacs) need += sizeof(float) * J * L;
   need += out_bytes + 8 * J + (64u << 20);
   // the device-memory query is skipped when this exact shape passed it before (all buffers exist)
@@ -669,7 +669,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(ctx->hd.ensure(sizeof(double) * J * n));
     CK(ctx->hidx.ensure(sizeof(uint32_t) * J * n));
   } else {
-    CK(ctx->mom.ensure(sizeof(double) * J * M * MOMW));
+    CK(ctx->mom.ensure(sizeof(Fix128) * J * nparts * M * MOMW));
   }
   CK(ctx->fb_list.ensure(4 * J));
   CK(ctx->fb_len.ensure(16));
@@ -843,7 +843,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     sp.LS = LS;
     sp.dist = ctx->cfg.distance;
     sp.unit_w = ctx->unit_w;
-    sp.mom = eps ? ctx->mom.as<double>() : nullptr;
+    sp.mom = eps ? ctx->mom.as<Fix128>() : nullptr;
     sp.eb = eb;
     sp.prior_g = ctx->d_prior.as<PriorDev>();
     sp.M = M;
@@ -866,7 +866,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     }
     sp.nparts = nparts;
     sp.bound_work = ctx->work.as<unsigned long long>() + 1;
-    if (eps) CK(cudaMemsetAsync(ctx->mom.p, 0, sizeof(double) * J * M * MOMW, st));
+    if (eps) CK(cudaMemsetAsync(ctx->mom.p, 0, sizeof(Fix128) * J * nparts * M * MOMW, st));
     // diagnostics: per-item timeline of the tree scan (env VPET_ITEMLOG=<file>)
     const char* ilog = tree ? getenv("VPET_ITEMLOG") : nullptr;
     const uint64_t nitems_dbg = ((J + 127) / 128) * nparts + 64;
@@ -932,7 +932,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   xp.bad = ctx->flag.as<int>();
 
   if (eps) {
-    EpsReduceParams ep{ctx->mom.as<double>(), J, ctx->prior, P, dout};
+    EpsReduceParams ep{ctx->mom.as<Fix128>(), nparts, J, ctx->prior, P, dout};
     launch_eps_reduce(ep, st);
     ++launches;
     rec(EV_CERT);
@@ -1135,6 +1135,66 @@ abc_status abc_response_envelope(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t
   EnvelopeParams ep{d_idx, J, ctx->N, n_acc, T, ctx->env_t.as<double>(), ctx->prior, d_q, ctx->flag.as<int>()};
   CK(launch_response_envelope(ep, st));
   if (!dev_out) CK(cudaMemcpyAsync(q, d_q, 12 * J * T, cudaMemcpyDeviceToHost, st));
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, ctx->flag.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (bad) return fail(ctx, ABC_E_ARG, "draw index out of range");
+  return ABC_OK;
+}
+
+abc_status abc_reduce_accepted(abc_ctx* ctx, const uint64_t* acc_idx, uint64_t J, uint32_t n_acc, uint32_t n_use,
+                               uint32_t ptr_flags, abc_result* out) {
+  if (!ctx || !out) return ABC_E_ARG;
+  if (ptr_flags & ~(ABC_PTR_TACS_DEVICE | ABC_PTR_OUT_DEVICE)) return fail(ctx, ABC_E_ARG, "unknown ptr_flags");
+  if (J == 0) return ABC_OK;
+  if (!acc_idx || n_acc == 0 || n_use == 0 || n_use > n_acc || n_use > 4096)
+    return fail(ctx, ABC_E_ARG, "need 1 <= n_use <= n_acc, n_use <= 4096");
+  if (out->acc_dist) return fail(ctx, ABC_E_ARG, "acc_dist is not produced by abc_reduce_accepted");
+  CK(cudaSetDevice(ctx->dev));
+  const cudaStream_t st = ctx->stream;
+  const uint32_t M = ctx->M, P = ctx->P;
+  const bool dev_idx = ptr_flags & ABC_PTR_TACS_DEVICE, host_out = !(ptr_flags & ABC_PTR_OUT_DEVICE);
+  const uint64_t* d_idx = acc_idx;
+  if (!dev_idx) {
+    CK(ctx->env_idx.ensure(8 * J * n_acc));
+    CK(cudaMemcpyAsync(ctx->env_idx.p, acc_idx, 8 * J * n_acc, cudaMemcpyHostToDevice, st));
+    d_idx = ctx->env_idx.as<uint64_t>();
+  }
+  struct OutDesc { void* user; size_t bytes; };
+  OutDesc od[10] = {{out->prob, 4 * J * M},       {out->preferred, 4 * J},  {out->count, 4 * J * M},
+                    {out->mean, 4 * J * P},       {out->sd, 4 * J * P},     {out->q, 12 * J * P},
+                    {out->ki_mean, 4 * J},        {out->ki_sd, 4 * J},      {out->ki_q, 12 * J},
+                    {out->acc_idx, 8 * J * n_use}};
+  abc_result dout = *out;
+  if (host_out) {
+    size_t tot = 0;
+    for (auto& d : od) if (d.user) tot += (d.bytes + 255) & ~size_t(255);
+    CK(ctx->env_q.ensure(tot ? tot : 16));
+    void** fields[10] = {(void**)&dout.prob, (void**)&dout.preferred, (void**)&dout.count, (void**)&dout.mean,
+                         (void**)&dout.sd,   (void**)&dout.q,         (void**)&dout.ki_mean, (void**)&dout.ki_sd,
+                         (void**)&dout.ki_q, (void**)&dout.acc_idx};
+    size_t off = 0;
+    for (int k = 0; k < 10; ++k) {
+      *fields[k] = od[k].user ? ctx->env_q.as<char>() + off : nullptr;
+      if (od[k].user) off += (od[k].bytes + 255) & ~size_t(255);
+    }
+  }
+  CK(ctx->flag.ensure(16));
+  CK(cudaMemsetAsync(ctx->flag.p, 0, 16, st));
+  ReduceParams rp{};
+  rp.J = J;
+  rp.n = n_use;
+  rp.N = ctx->N;
+  rp.prior = ctx->prior;
+  rp.P = P;
+  rp.out = dout;
+  CK(launch_reduce_list(rp, d_idx, n_acc, ctx->flag.as<int>(), st));
+  if (host_out) {
+    void* srcs[10] = {dout.prob, dout.preferred, dout.count, dout.mean, dout.sd, dout.q,
+                      dout.ki_mean, dout.ki_sd, dout.ki_q, dout.acc_idx};
+    for (int k = 0; k < 10; ++k)
+      if (od[k].user) CK(cudaMemcpyAsync(od[k].user, srcs[k], od[k].bytes, cudaMemcpyDeviceToHost, st));
+  }
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, ctx->flag.p, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

@@ -186,7 +186,7 @@ __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* c
   const abc_result& o = p.out;
   for (uint32_t a = lane; a < n; a += 32) {
     if (o.acc_idx) o.acc_idx[v * n + a] = ci[a];
-    if (o.acc_dist) o.acc_dist[v * n + a] = cd[a];
+    if (o.acc_dist && cd) o.acc_dist[v * n + a] = cd[a];
   }
   uint32_t cnt[ABC_MAX_MODELS] = {0, 0, 0, 0};
   for (uint32_t base = 0; base < n; base += 32) {
@@ -495,32 +495,37 @@ __global__ void eps_reduce_kernel(const EpsReduceParams p) {
   uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= p.J) return;
   const uint32_t M = p.prior.M;
-  const double* mom = p.mom + v * size_t(M) * MOMW;
   const abc_result& o = p.out;
   const float NANF = __int_as_float(0x7fc00000);
+  // sum the parts' fixed-point sums (exact), then convert once
+  auto total = [&](uint32_t m, uint32_t slot) {
+    Fix128 a = 0;
+    for (uint32_t q = 0; q < p.nparts; ++q) a += p.mom[((v * p.nparts + q) * M + m) * MOMW + slot];
+    return from_fix(a);
+  };
   double tot = 0.0;
   int pref = -1;
   double best = -1.0;
   for (uint32_t m = 0; m < M; ++m) {
-    double c = mom[m * MOMW];
+    double c = total(m, 0);
     tot += c;
     if (c > best) { best = c; pref = int(m); }
   }
   if (tot == 0.0) pref = -1;
   for (uint32_t m = 0; m < M; ++m) {
-    double c = mom[m * MOMW];
+    double c = total(m, 0);
     if (o.count) o.count[v * M + m] = uint32_t(c);
     if (o.prob) o.prob[v * M + m] = tot > 0.0 ? float(c / tot) : NANF;
   }
   if (o.preferred) o.preferred[v] = pref;
   int kind = pref >= 0 ? p.prior.m[pref].kind : p.prior.m[0].kind;
-  double c = pref >= 0 ? mom[pref * MOMW] : 0.0;
-  const double* s = pref >= 0 ? mom + pref * MOMW : mom;
+  const uint32_t pm = pref >= 0 ? uint32_t(pref) : 0u;
+  double c = pref >= 0 ? total(pm, 0) : 0.0;
   for (uint32_t k = 0; k < p.P; ++k) {
     float mean = NANF, sd = NANF;
     if (c > 0.0 && column_exists(kind, k)) {
       double lo = p.prior.m[pref].lo[k];
-      double s1 = s[1 + 2 * k], s2 = s[2 + 2 * k];
+      double s1 = total(pm, 1 + 2 * k), s2 = total(pm, 2 + 2 * k);
       mean = float(lo + s1 / c);
       if (c >= 2.0) sd = float(sqrt(fmax(s2 - s1 * s1 / c, 0.0) / (c - 1.0)));
     }
@@ -530,13 +535,37 @@ __global__ void eps_reduce_kernel(const EpsReduceParams p) {
   }
   float km = NANF, ks = NANF;
   if (c > 0.0 && kind <= ABC_2TCM_REV) {
-    double s1 = s[1 + 2 * ABC_MAX_P], s2 = s[2 + 2 * ABC_MAX_P];
+    double s1 = total(pm, 1 + 2 * ABC_MAX_P), s2 = total(pm, 2 + 2 * ABC_MAX_P);
     km = float(s1 / c);
     if (c >= 2.0) ks = float(sqrt(fmax(s2 - s1 * s1 / c, 0.0) / (c - 1.0)));
   }
   if (o.ki_mean) o.ki_mean[v] = km;
   if (o.ki_sd) o.ki_sd[v] = ks;
   if (o.ki_q) for (int t = 0; t < 3; ++t) o.ki_q[v * 3 + t] = NANF;
+}
+
+// ---- posterior summaries of given accepted lists (abc_reduce_accepted) ----------------------
+// Warp per voxel: the first n_use indices of the voxel's list (e.g. a top-n list sorted by (D, i):
+// its prefix IS the top-n_use set of the same run, SURVEY §8f-3 "truncation of one max-n run")
+// are reduced exactly as K4 reduces a certified list.
+__global__ void reduce_list_kernel(const ReduceParams p, const uint64_t* idx, uint32_t n_acc, uint32_t np2, uint32_t wpc,
+                                   int* bad) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const uint32_t w = threadIdx.x >> 5;
+  const size_t per_warp = size_t(np2) * 12;
+  double* sc = reinterpret_cast<double*>(smem_raw + per_warp * w);
+  uint32_t* ci = reinterpret_cast<uint32_t*>(sc + np2);
+  for (uint64_t v = uint64_t(blockIdx.x) * wpc + w; v < p.J; v += uint64_t(gridDim.x) * wpc) {
+    for (uint32_t a = lane; a < p.n; a += 32) {
+      const uint64_t i = idx[v * n_acc + a];
+      if (i >= p.N) atomicExch(bad, 1);
+      ci[a] = uint32_t(i < p.N ? i : 0);
+    }
+    __syncwarp();
+    reduce_topn(p, v, ci, nullptr, sc, np2, lane);
+    __syncwarp();
+  }
 }
 
 uint32_t next_pow2(uint32_t x) {
@@ -650,6 +679,22 @@ void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st) {
   uint64_t blocks = (p.J + 127) / 128;
   if (blocks == 0) return;
   eps_reduce_kernel<<<unsigned(blocks), 128, 0, st>>>(p);
+}
+
+cudaError_t launch_reduce_list(const ReduceParams& p, const uint64_t* idx, uint32_t n_acc, int* bad, cudaStream_t st) {
+  uint32_t np2 = next_pow2(p.n);
+  if (np2 < 32) np2 = 32;
+  const size_t per_warp = size_t(np2) * 12;
+  uint32_t wpc = 8;
+  while (wpc > 1 && per_warp * wpc > 96 * 1024) wpc >>= 1;
+  const size_t smem = per_warp * wpc;
+  cudaError_t e = ensure_smem_attr((const void*)reduce_list_kernel, smem);
+  if (e != cudaSuccess) return e;
+  uint64_t blocks = (p.J + wpc - 1) / wpc;
+  if (blocks > 148ull * 32) blocks = 148ull * 32;
+  if (blocks == 0) blocks = 1;
+  reduce_list_kernel<<<unsigned(blocks), wpc * 32, smem, st>>>(p, idx, n_acc, np2, wpc, bad);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_response_envelope(const EnvelopeParams& p, cudaStream_t st) {

@@ -1,6 +1,7 @@
 // common.cuh -- device-side building blocks shared by the kernels of libvpetabc.so.
 // (Independent of oracle/: nothing here is shared with the CPU oracle.)
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -23,6 +24,30 @@ constexpr int kNPC = VPET_NPC;  // principal axes used for the draw order (order
 constexpr int kTile = VPET_TILE;    // draws per tile (bounding box + TMA transfer unit)
 constexpr int kSuper = VPET_SUPER;  // tiles per super-tile (<= 32: one bit per tile in a mask)
 constexpr int kMaxGrid = 8192;  // max points of a draw-independent time grid
+// ---------------------------------------------------------------------------------------
+// Eps-mode moment sums in 128-bit fixed point (kFixFrac fractional bits).  Each accepted draw's
+// value is rounded once to the grid 2^-62 (deterministically, per draw); integer sums are then
+// exact and associative, so the result does not depend on the order in which the FP32 pass
+// visits the draws (which depends on the voxel's CTA-mates, i.e. on the sharding).
+// Range: |value| < 2^53, sums < 2^64 (count <= 2^32, values < 2^31): < 2^126.
+// ---------------------------------------------------------------------------------------
+typedef __int128 Fix128;
+constexpr int kFixFrac = 62;
+__host__ __device__ inline Fix128 to_fix(double v) {
+  const double ip = trunc(v);
+  const double r = v - ip;  // exact, |r| < 1
+#ifdef __CUDA_ARCH__
+  const long long f = __double2ll_rn(r * 4611686018427387904.0);  // r 2^62 (exact scaling)
+#else
+  const long long f = llrint(r * 4611686018427387904.0);
+#endif
+  return (Fix128((long long)ip) << kFixFrac) + Fix128(f);
+}
+__host__ __device__ inline double from_fix(Fix128 a) {
+  const long long hi = (long long)(a >> kFixFrac);  // floor
+  const unsigned long long lo = (unsigned long long)(a & ((Fix128(1) << kFixFrac) - 1));
+  return double(hi) + double(lo) * 2.168404344971008868e-19;  // 2^-62
+}
 
 // ---------------------------------------------------------------------------------------
 // Prior draw (Alg.1 l.1-2): Philox4x32-10 keyed by the seed, counter
@@ -256,7 +281,7 @@ struct ScanParams {
   uint32_t LS;
   int dist;             // ABC_DIST_*
   int unit_w;
-  double* mom;          // [J][M][MOMW] eps-mode moment sums
+  Fix128* mom;          // [J][nparts][M][MOMW] eps-mode moment sums (fixed point, one owner per slot)
   ErrBound eb;
   const PriorDev* prior_g;  // device copy of the prior (eps-mode slow path)
   uint32_t M;
@@ -343,6 +368,8 @@ struct ReduceParams {
   abc_result out;
 };
 cudaError_t launch_certify_reduce(const ReduceParams& p, cudaStream_t st);
+// K4 on given accepted lists (abc_reduce_accepted): the first p.n of n_acc indices per voxel.
+cudaError_t launch_reduce_list(const ReduceParams& p, const uint64_t* idx, uint32_t n_acc, int* bad, cudaStream_t st);
 
 // Response-function envelope (Fig. 1): abc_response_envelope.
 struct EnvelopeParams {
@@ -371,7 +398,8 @@ struct PatlakParams {
 void launch_patlak(const PatlakParams& p, cudaStream_t st);
 
 struct EpsReduceParams {
-  const double* mom;
+  const Fix128* mom;    // [J][nparts][M][MOMW]
+  uint32_t nparts;
   uint64_t J;
   PriorDev prior;
   uint32_t P;

@@ -243,26 +243,27 @@ __device__ __forceinline__ double exact_distance(const float* y, const float* s,
   return D;
 }
 
-// Eps mode: exact re-score of a candidate; accepted draws update the voxel's moment sums.
+// Eps mode: exact re-score of a candidate; accepted draws update the voxel's moment sums of this
+// part (mom points at [M][MOMW] of (voxel, part): one owner thread at a time, no atomics).
 static __device__ __noinline__ void eps_candidate(const float* yrow, const float* bank, uint32_t LS, const float* w,
-                                           uint32_t L, int dist, double eps, double* mom, const PriorDev* prior,
+                                           uint32_t L, int dist, double eps, Fix128* mom, const PriorDev* prior,
                                            uint64_t i) {
   double D = exact_distance(yrow, bank + i * LS, w, L, dist);
   if (!(D <= eps)) return;
   float th[ABC_MAX_P];
   int m = draw_theta(*prior, i, th);
   const ModelDev& md = prior->m[m];
-  double* s = mom + size_t(m) * MOMW;  // parts of one voxel may run concurrently: atomics
-  atomicAdd(s, 1.0);
+  Fix128* s = mom + size_t(m) * MOMW;
+  s[0] += Fix128(1) << kFixFrac;
   for (uint32_t k = 0; k < md.P; ++k) {
     double x = double(th[k]) - double(md.lo[k]);
-    atomicAdd(s + 1 + 2 * k, x);
-    atomicAdd(s + 2 + 2 * k, x * x);
+    s[1 + 2 * k] += to_fix(x);
+    s[2 + 2 * k] += to_fix(x * x);
   }
   if (md.kind <= ABC_2TCM_REV) {
     double ki = double(th[0]) * double(th[2]) / (double(th[1]) + double(th[2]));
-    atomicAdd(s + 1 + 2 * ABC_MAX_P, ki);
-    atomicAdd(s + 2 + 2 * ABC_MAX_P, ki * ki);
+    s[1 + 2 * ABC_MAX_P] += to_fix(ki);
+    s[2 + 2 * ABC_MAX_P] += to_fix(ki * ki);
   }
 }
 
@@ -422,7 +423,7 @@ __device__ __forceinline__ void finish_row(const ScanParams& p, Voxels<LP, R>& V
         V.tau[r] = fminf(V.tau[r], V.taup[r]);
       } else {
         eps_candidate(p.tacs + uint64_t(V.vox[r]) * p.L, p.bank, p.LS, p.w, p.L, p.dist, p.eps,
-                      p.mom + uint64_t(V.vox[r]) * (size_t(p.M) * MOMW), p.prior_g, i);
+                      p.mom + (uint64_t(V.vox[r]) * p.nparts + part) * (size_t(p.M) * MOMW), p.prior_g, i);
       }
     }
   }

@@ -68,7 +68,7 @@ def gather_maps(local: dict, J: int, device, dst: int = 0, names: Optional[Itera
     host or device).  Returns {name: full J-row tensor on `device`} on `dst`, None elsewhere.
     Shards are padded to the largest shard so every rank sends one fixed-size buffer per field.
     """
-    world, rank = dist.get_world_size(), dist.get_rank()
+    world, rank = (dist.get_world_size(), dist.get_rank()) if dist.is_initialized() else (1, 0)
     mx = shard_size(J, world, 0)
     out = {}
     for name in sorted(names if names is not None else local):
@@ -116,8 +116,12 @@ def run_volume(ctx, tacs_shard, J: int, dst: int = 0, names=MAP_OUTPUTS, out=Non
     res = ctx.run_voxels(tacs_shard, want=tuple(names), out=out)
     if isinstance(tacs_shard, torch.Tensor) and tacs_shard.is_cuda:
         dev = tacs_shard.device
+    elif out is not None and any(isinstance(v, torch.Tensor) and v.is_cuda for v in out.values()):
+        dev = next(v.device for v in out.values() if isinstance(v, torch.Tensor))
+    elif dist.is_initialized() and dist.get_backend() == "nccl":
+        dev = torch.device("cuda", torch.cuda.current_device())
     else:
-        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+        dev = torch.device("cpu")
     return gather_maps({k: res[k] for k in names}, J, dev, dst=dst, names=names)
 
 

@@ -292,3 +292,42 @@ def test_nonfinite_voxel_returns_quickly(tb_small):
     assert t_bad < max(2.0 * t_ok, 0.2), (t_bad, t_ok)
     r = ctx.run_voxels(p.tacs)  # the context stays usable
     assert np.all(np.isfinite(r["ki_mean"]))
+
+
+def test_truncation_equals_direct_runs(rt_small):
+    """the summaries of the first n' entries of a top-n run's sorted accepted lists
+    (abc_reduce_accepted) are those of a direct top-n' run, byte for byte (P:170-175 pilot sweep)."""
+    import torch
+    from paper_2603_14859_b200 import AbcContext
+    big = rt_small.replace(n_accept=100)
+    ctx = AbcContext(**big.ctx_kwargs)
+    big.setup(ctx)
+    full = ctx.run_voxels(big.tacs)
+    dfull = ctx.run_voxels(torch.from_numpy(big.tacs).cuda())
+    for n in (15, 50, 100):
+        d, _ = run_gpu(rt_small.replace(n_accept=n))
+        t = ctx.reduce_accepted(full["acc_idx"], n, want=tuple(k for k in d if k != "acc_dist"))
+        td = ctx.reduce_accepted(dfull["acc_idx"], n)
+        for k in t:
+            np.testing.assert_array_equal(np.nan_to_num(t[k]), np.nan_to_num(d[k]), err_msg=(n, k))
+        for k in td:
+            a = td[k].cpu().numpy()
+            if d[k].dtype == np.uint32:
+                a = a.view(np.uint32)
+            np.testing.assert_array_equal(np.nan_to_num(a), np.nan_to_num(d[k]), err_msg=(n, k))
+
+
+def test_epsilon_calibrated_from_pilot(tb_small):
+    """calibrate.epsilon_from_pilot: eps = median over voxels of the pilot's n-th smallest D makes
+    about half of the voxels accept >= n draws in eps mode, and each voxel's
+    eps-mode count is exactly the number of its pilot distances <= eps (below the pilot's n_max)."""
+    from paper_2603_14859_b200 import calibrate as CAL
+    p = tb_small.replace(n_accept=60)
+    g, _ = run_gpu(p)
+    eps = CAL.epsilon_from_pilot(g["acc_dist"], 18)
+    e, _ = run_gpu(p.replace(accept="EPS", epsilon=eps))
+    cnt = e["count"].sum(1).astype(np.int64)
+    frac = np.mean(cnt >= 18)
+    assert 0.5 <= frac <= 0.5 + 2.0 / p.J, frac
+    below = cnt < 60
+    np.testing.assert_array_equal(cnt[below], np.sum(g["acc_dist"][below] <= eps, axis=1))

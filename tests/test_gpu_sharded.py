@@ -105,3 +105,25 @@ def test_world1_nccl_run_volume_device_path():
             assert torch.equal(maps_h[k], maps[k]), k
     finally:
         dist.destroy_process_group()
+
+
+def test_eps_mode_sharding_invariant():
+    """eps mode sums the accepted draws' moments in 128-bit fixed point per (voxel,
+    part): the maps of an interleaved shard are byte-identical to those of the full run although
+    the FP32 pass visits the draws in a different order (other CTA-mates)."""
+    from paper_2603_14859_b200 import AbcContext
+    from paper_2603_14859_b200.distributed import shard_indices
+    from tests.parity import run_oracle
+    p = S.config4_chunk(chunk=9, n_chunks=64, N=100_000, n=18, max_voxels=1500)
+    o_top, _ = run_oracle(p.subset(np.arange(40)))
+    eps = float(np.median(o_top["acc_dist"][:, -1]))
+    q = p.replace(accept="EPS", epsilon=eps)
+    ctx = AbcContext(**q.ctx_kwargs)
+    q.setup(ctx)
+    full = ctx.run_voxels(q.tacs)
+    for world in (2, 3):
+        for r in range(world):
+            idx = shard_indices(q.J, world, r)
+            part = ctx.run_voxels(np.ascontiguousarray(q.tacs[idx]))
+            for k in part:
+                np.testing.assert_array_equal(part[k].view(np.uint8), full[k][idx].view(np.uint8), err_msg=k)
