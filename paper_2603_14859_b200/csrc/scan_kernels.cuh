@@ -315,9 +315,44 @@ __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& 
   }
 }
 
+// Per-voxel accumulator of the FP32 pass: float2 chains (even / odd frames).  VPET_ACC2 = 1 uses two
+// float2 chains (frames 4q, 4q+1 and 4q+2, 4q+3): half the dependent FFMA2 latency per chunk, two
+// more registers per voxel.  Every chain only grows (non-negative terms, monotone rounding), so any
+// prefix total is <= the final D32 (exact pruning), and the total is a sum of the L terms in a
+// tree of height < L (the gamma_L error bound holds).
+#ifndef VPET_ACC2
+#define VPET_ACC2 0
+#endif
+struct Acc {
+  float2 a;
+#if VPET_ACC2
+  float2 b;
+#endif
+};
+__device__ __forceinline__ void acc_zero(Acc& c) {
+  c.a = make_float2(0.0f, 0.0f);
+#if VPET_ACC2
+  c.b = make_float2(0.0f, 0.0f);
+#endif
+}
+__device__ __forceinline__ float acc_total(const Acc& c) {
+#if VPET_ACC2
+  return __fadd_rn(__fadd_rn(c.a.x, c.a.y), __fadd_rn(c.b.x, c.b.y));
+#else
+  return __fadd_rn(c.a.x, c.a.y);
+#endif
+}
+__device__ __forceinline__ float2& acc_second(Acc& c) {
+#if VPET_ACC2
+  return c.b;
+#else
+  return c.a;
+#endif
+}
+
 // Chunk [c*CH, min((c+1)*CH, LP)) of the distance of R voxels to one bank row (scan order).
 template <int LP, int R, int DIST, int C>
-__device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const float* sr, float2 (&acc)[R]) {
+__device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const float* sr, Acc (&acc)[R]) {
 #pragma unroll
   for (int q = C * CH; q < ((C + 1) * CH < LP ? (C + 1) * CH : LP); q += 4) {
     const float4 s4 = *reinterpret_cast<const float4*>(sr + q);
@@ -328,13 +363,13 @@ __device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const float* 
       float2 d0 = __fadd2_rn(V.y[r][q / 2], sa);
       float2 d1 = __fadd2_rn(V.y[r][q / 2 + 1], sc);
       if (DIST == ABC_DIST_WL2) {
-        acc[r] = __ffma2_rn(d0, d0, acc[r]);
-        acc[r] = __ffma2_rn(d1, d1, acc[r]);
+        acc[r].a = __ffma2_rn(d0, d0, acc[r].a);
+        acc_second(acc[r]) = __ffma2_rn(d1, d1, acc_second(acc[r]));
       } else {
-        acc[r].x = __fadd_rn(acc[r].x, fabsf(d0.x));
-        acc[r].y = __fadd_rn(acc[r].y, fabsf(d0.y));
-        acc[r].x = __fadd_rn(acc[r].x, fabsf(d1.x));
-        acc[r].y = __fadd_rn(acc[r].y, fabsf(d1.y));
+        acc[r].a.x = __fadd_rn(acc[r].a.x, fabsf(d0.x));
+        acc[r].a.y = __fadd_rn(acc[r].a.y, fabsf(d0.y));
+        acc_second(acc[r]).x = __fadd_rn(acc_second(acc[r]).x, fabsf(d1.x));
+        acc_second(acc[r]).y = __fadd_rn(acc_second(acc[r]).y, fabsf(d1.y));
       }
     }
   }
@@ -343,7 +378,7 @@ __device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const float* 
 // Same chunk of the lower bound against a box [lo, hi] of bankp values (global memory).
 template <int LP, int R, int DIST, int C>
 __device__ __forceinline__ void bound_chunk(const Voxels<LP, R>& V, const float* lo, const float* hi,
-                                            float2 (&acc)[R]) {
+                                            Acc (&acc)[R]) {
 #pragma unroll
   for (int q = C * CH; q < ((C + 1) * CH < LP ? (C + 1) * CH : LP); q += 4) {
     // generic loads: the boxes live in shared memory (prefetched super/tile boxes) or global memory
@@ -359,23 +394,23 @@ __device__ __forceinline__ void bound_chunk(const Voxels<LP, R>& V, const float*
       float2 g0 = make_float2(fmaxf(fmaxf(a0.x, -b0.x), 0.0f), fmaxf(fmaxf(a0.y, -b0.y), 0.0f));
       float2 g1 = make_float2(fmaxf(fmaxf(a1.x, -b1.x), 0.0f), fmaxf(fmaxf(a1.y, -b1.y), 0.0f));
       if (DIST == ABC_DIST_WL2) {
-        acc[r] = __ffma2_rn(g0, g0, acc[r]);
-        acc[r] = __ffma2_rn(g1, g1, acc[r]);
+        acc[r].a = __ffma2_rn(g0, g0, acc[r].a);
+        acc_second(acc[r]) = __ffma2_rn(g1, g1, acc_second(acc[r]));
       } else {
-        acc[r].x = __fadd_rn(acc[r].x, g0.x);
-        acc[r].y = __fadd_rn(acc[r].y, g0.y);
-        acc[r].x = __fadd_rn(acc[r].x, g1.x);
-        acc[r].y = __fadd_rn(acc[r].y, g1.y);
+        acc[r].a.x = __fadd_rn(acc[r].a.x, g0.x);
+        acc[r].a.y = __fadd_rn(acc[r].a.y, g0.y);
+        acc_second(acc[r]).x = __fadd_rn(acc_second(acc[r]).x, g1.x);
+        acc_second(acc[r]).y = __fadd_rn(acc_second(acc[r]).y, g1.y);
       }
     }
   }
 }
 
 template <int LP, int R>
-__device__ __forceinline__ bool any_alive(const Voxels<LP, R>& V, const float2 (&acc)[R], bool noprune) {
+__device__ __forceinline__ bool any_alive(const Voxels<LP, R>& V, const Acc (&acc)[R], bool noprune) {
   bool alive = noprune;
 #pragma unroll
-  for (int r = 0; r < R; ++r) alive |= (__fadd_rn(acc[r].x, acc[r].y) < V.tau[r]);
+  for (int r = 0; r < R; ++r) alive |= (acc_total(acc[r]) < V.tau[r]);
   return __any_sync(0xffffffffu, alive);
 }
 
@@ -383,7 +418,7 @@ __device__ __forceinline__ bool any_alive(const Voxels<LP, R>& V, const float2 (
 template <int LP, int R, int DIST, bool BOUND, int C>
 struct Chunks {
   static constexpr int NCH = (LP + CH - 1) / CH;
-  __device__ __forceinline__ static bool run(const Voxels<LP, R>& V, const float* a, const float* b, float2 (&acc)[R],
+  __device__ __forceinline__ static bool run(const Voxels<LP, R>& V, const float* a, const float* b, Acc (&acc)[R],
                                              unsigned long long& work, bool noprune) {
     if (BOUND) bound_chunk<LP, R, DIST, C>(V, a, b, acc);
     else dist_chunk<LP, R, DIST, C>(V, a, acc);
@@ -403,11 +438,11 @@ struct Chunks {
 #endif
 // Insert the survivors of draw i (full D32 in acc) into the lanes' candidate heaps.
 template <int LP, int R, bool COUNT, bool SH>
-__device__ __forceinline__ void finish_row(const ScanParams& p, Voxels<LP, R>& V, const float2 (&acc)[R], uint64_t i,
+__device__ __forceinline__ void finish_row(const ScanParams& p, Voxels<LP, R>& V, const Acc (&acc)[R], uint64_t i,
                                            uint32_t part, unsigned long long& work, uint32_t htop_s) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    float D = __fadd_rn(acc[r].x, acc[r].y);
+    float D = acc_total(acc[r]);
     if (VPET_PUSHCHECK && D < V.tau[r] && !p.eps_mode && p.tau_glob)
       V.tau[r] = fminf(V.tau[r], __uint_as_float(__ldcg(p.tau_glob + V.vox[r])));
     if (D < V.tau[r]) {
@@ -432,9 +467,9 @@ __device__ __forceinline__ void finish_row(const ScanParams& p, Voxels<LP, R>& V
 template <int LP, int R, int DIST, bool COUNT, bool SH = false>
 __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, const float* sr, uint64_t i,
                                          uint32_t part, unsigned long long& work, uint32_t htop_s = 0) {
-  float2 acc[R];
+  Acc acc[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
+  for (int r = 0; r < R; ++r) acc_zero(acc[r]);
   unsigned long long w = 0;
   bool go = Chunks<LP, R, DIST, false, 0>::run(V, sr, nullptr, acc, w, !p.prune);
   if (COUNT && !VPET_COUNT_PUSH) work += w;
@@ -449,11 +484,11 @@ __device__ __forceinline__ void eval_pair(const ScanParams& p, Voxels<LP, R>& V,
                                           const float* sb, uint64_t ib, uint32_t part, unsigned long long& work,
                                           uint32_t htop_s = 0) {
   constexpr int NCH = (LP + CH - 1) / CH;
-  float2 aa[R], ab[R];
+  Acc aa[R], ab[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    aa[r] = make_float2(0.0f, 0.0f);
-    ab[r] = make_float2(0.0f, 0.0f);
+    acc_zero(aa[r]);
+    acc_zero(ab[r]);
   }
   dist_chunk<LP, R, DIST, 0>(V, sa, aa);
   dist_chunk<LP, R, DIST, 0>(V, sb, ab);
@@ -499,9 +534,9 @@ __device__ __forceinline__ void refresh_tau_pipe(const ScanParams& p, Voxels<LP,
 
 template <int LP, int R, int DIST>
 __device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const float* box, unsigned long long& work) {
-  float2 acc[R];
+  Acc acc[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = make_float2(0.0f, 0.0f);
+  for (int r = 0; r < R; ++r) acc_zero(acc[r]);
   return Chunks<LP, R, DIST, true, 0>::run(V, box, box + LP, acc, work, false);
 }
 
