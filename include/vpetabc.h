@@ -91,7 +91,7 @@ typedef enum { ABC_INPUT_PWL = 0, ABC_INPUT_FENG = 1 } abc_input_kind;
 #define ABC_FLAG_NO_TREE 0x20u   /* FP32 pass scans every draw in index order, no bounds (A/B only) */
 #define ABC_FLAG_DENSE_TC 0x40u  /* replace the FP32 pass by the dense shared-bank tensor-core
                                     distance (y.s cross term on tcgen05, BF16x3 split; WL2, TOPN,
-                                    L <= 48, else ABC_E_UNSUPPORTED).  Same certified results;
+                                    L <= 48, n <= 2032, else ABC_E_UNSUPPORTED).  Same certified results;
                                     evaluates every pair (SURVEY.md §8f-1, A/B comparison) */
 #define ABC_FLAG_FORCE_FALLBACK 0x80u /* test hook: certification rejects every voxel, so every
                                     voxel is re-run by the exact FP64 scan (the uncertified-voxel
@@ -117,7 +117,7 @@ typedef struct abc_config {
   int32_t device;         /* CUDA device ordinal */
   int32_t distance;       /* abc_distance */
   int32_t accept;         /* abc_accept */
-  uint32_t n_accept;      /* n for TOPN: 1 <= n <= N, n <= 4096 (n = floor(N p)) */
+  uint32_t n_accept;      /* n for TOPN: 1 <= n <= N, n <= 15360 (n = floor(N p)) */
   double epsilon;         /* tolerance h for EPS, >= 0 */
   double lpnt_step_min;   /* lp-ntPET integrator step delta (min); <= 0 selects 0.05 */
   uint32_t flags;         /* ABC_FLAG_* */
@@ -162,7 +162,7 @@ typedef struct abc_ctx abc_ctx; /* opaque, library-owned */
 /* Create a context on cfg->device.  ABC_E_ARG: struct_size mismatch, M out of range,
  * mixed model families, N_m = 0, N = sum N_m >= 2^32, lo > hi or non-finite bounds,
  * 2TCM with lo[k3] <= 0 (R3), unknown distance/accept, TOPN with n = 0,
- * n > N or n > 4096, EPS with epsilon < 0 or NaN, reserved fields != 0.
+ * n > N or n > 15360, EPS with epsilon < 0 or NaN, reserved fields != 0.
  * ABC_E_CUDA: the device cannot be selected.  *out is NULL on failure. */
 abc_status abc_init(const abc_config* cfg, abc_ctx** out);
 

@@ -401,7 +401,7 @@ abc_status abc_init(const abc_config* cfg, abc_ctx** out) {
   if (N >= (1ull << 32)) return ABC_E_ARG;
   if (cfg->distance != ABC_DIST_L1 && cfg->distance != ABC_DIST_WL2) return ABC_E_ARG;
   if (cfg->accept == ABC_ACCEPT_TOPN) {
-    if (cfg->n_accept == 0 || cfg->n_accept > N || cfg->n_accept > 4096) return ABC_E_ARG;
+    if (cfg->n_accept == 0 || cfg->n_accept > N || cfg->n_accept > kMaxAccept) return ABC_E_ARG;
   } else if (cfg->accept == ABC_ACCEPT_EPS) {
     if (!(cfg->epsilon >= 0.0)) return ABC_E_ARG;
   } else {
@@ -557,8 +557,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const bool timing = (ctx->cfg.flags & ABC_FLAG_TIMING) && ctx->ev_ok;
   const bool count_work = (ctx->cfg.flags & ABC_FLAG_COUNT_WORK) != 0;
   const bool dense = (ctx->cfg.flags & ABC_FLAG_DENSE_TC) && !exact;
-  if (dense && (eps || !ctx->dist_wl2() || L > 48))
-    return fail(ctx, ABC_E_UNSUPPORTED, "ABC_FLAG_DENSE_TC needs WL2, top-n acceptance and L <= 48");
+  if (dense && (eps || !ctx->dist_wl2() || L > 48 || 2 * (4 * uint64_t(ctx->cfg.n_accept) + 64) > kLargeMaxCand))
+    return fail(ctx, ABC_E_UNSUPPORTED, "ABC_FLAG_DENSE_TC needs WL2, top-n acceptance, L <= 48 and n <= 2032");
   const uint32_t n = ctx->cfg.n_accept;
   uint32_t K = 0;
   if (!eps) {
@@ -594,7 +594,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
   // draw-range split of the tree scan (interleaved super-tiles): balances heavy voxels over SMs
   uint32_t nparts = 1;
-  if (tree && !eps) nparts = K <= 512 ? 6u : 2u;
+  // parts share the draws of a voxel between SMs; each keeps its own K candidates, so large n uses
+  // fewer parts (certification holds all parts' candidates of a voxel in shared memory)
+  if (tree && !eps) nparts = K <= 512 ? 6u : (2 * K <= kLargeMaxCand ? 2u : 1u);
   if (tree && eps) nparts = 6u;
   if (const char* e = getenv("VPET_NPARTS")) nparts = uint32_t(std::max(1, atoi(e)));  // tuning knob
   // hyper-tiles of hs super-tiles: the unit of the work split and of the best-first order; at most

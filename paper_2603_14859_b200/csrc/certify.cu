@@ -401,6 +401,288 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
   }
 }
 
+// =============================================================================================
+// Large-n certification + reduction (K3/K4 for n up to kMaxAccept): one CTA of kLT threads per
+// voxel, candidates in shared memory (up to kLargeMaxCand (D64, i) pairs = 196 KB), a CTA-wide
+// bitonic sort of the candidates by (D64, i), and per-column type-7 quantiles by CTA radix select
+// (8-bit digits of order-preserving 64-bit keys) instead of sorts.  Same arithmetic and same
+// certification test as the warp path (certify_reduce_kernel); only the parallel layout differs.
+// =============================================================================================
+constexpr int kLT = 512;
+
+__device__ __forceinline__ uint64_t okey(double x) {  // order-preserving map of an FP64 value
+  const uint64_t u = uint64_t(__double_as_longlong(x));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double okey_inv(uint64_t k) {
+  const uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+// Ascending bitonic sort of n2 (power of two) (key, idx) pairs by (key, idx), whole CTA.
+__device__ void cta_sort_pairs(double* key, uint32_t* idx, uint32_t n2) {
+  for (uint32_t size = 2; size <= n2; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t t = threadIdx.x; t < n2 / 2; t += blockDim.x) {
+        const uint32_t i = 2 * t - (t & (stride - 1)), j = i + stride;
+        const bool asc = (i & size) == 0;
+        const double a = key[i], b = key[j];
+        const uint32_t ia = idx[i], ib = idx[j];
+        if (pair_gt(a, ia, b, ib) == asc) {
+          key[i] = b; key[j] = a;
+          idx[i] = ib; idx[j] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Value of rank r (0-based) among kv[0..c) (uint64 keys), whole CTA; hist: 256 words, bc: 2 words.
+__device__ uint64_t cta_select(const uint64_t* kv, uint32_t c, uint32_t r, uint32_t* hist, uint32_t* bc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t prefix = 0, decided = 0;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (uint32_t a = threadIdx.x; a < c; a += blockDim.x) {
+      const uint64_t k = kv[a];
+      if ((k & decided) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t h[8], s = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { h[q] = hist[lane * 8 + q]; s += h[q]; }
+      uint32_t inc = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      const uint32_t exc = inc - s;
+      if (exc <= r && r < inc) {
+        uint32_t acc = exc;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (r < acc + h[q]) { bc[0] = uint32_t(lane * 8 + q); bc[1] = r - acc; break; }
+          acc += h[q];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= uint64_t(bc[0]) << shift;
+    decided |= uint64_t(255) << shift;
+    r = bc[1];
+    __syncthreads();
+  }
+  return prefix;
+}
+
+__device__ __forceinline__ double cta_sum(double x, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  x = warp_sum(x);
+  __syncthreads();
+  if (lane == 0) red[warp] = x;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];  // fixed order: deterministic
+  return t;
+}
+
+// theta columns of the Philox block that holds column k (one Philox4x32-10 call): block 0 = columns
+// 0-3, block 1 = columns 4-7; same values as draw_theta (common.cuh).
+__device__ __forceinline__ void theta_block(const PriorDev& pr, uint64_t i, int m, uint32_t blk, float th[ABC_MAX_P]) {
+  const ModelDev& md = pr.m[m];
+  uint32_t w[4];
+  philox10(uint32_t(i), uint32_t(i >> 32), blk, kCtrTag, pr.seed_lo, pr.seed_hi, w);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = int(blk) * 4 + q;
+    th[k] = (k < (int)md.P) ? fmaf(md.span[k], u01(w[q]), md.lo[k]) : 0.0f;
+  }
+  if (blk == 0 && (md.kind == ABC_2TCM_IRR || md.kind == ABC_MRTM)) th[3] = 0.0f;
+  if (blk == 1 && md.kind >= ABC_MRTM) th[5] = __fadd_rn(th[4], th[5]);
+}
+
+__global__ void __launch_bounds__(kLT, 1) certify_large_kernel(const ReduceParams p, uint32_t Kp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* cd = reinterpret_cast<double*>(smem_raw);          // [Kp] D64 (later: uint64 value keys)
+  uint32_t* ci = reinterpret_cast<uint32_t*>(cd + Kp);       // [Kp] draw indices
+  uint32_t* hist = ci + Kp;                                  // [256]
+  uint32_t* sc = hist + 256;                                 // [16] counters / broadcasts
+  double* red = reinterpret_cast<double*>(sc + 16);          // [kLT / 32]
+  if (p.bad && *p.bad) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t len = p.list_len ? uint64_t(*p.list_len) : p.J;
+  const double DINF = __longlong_as_double(0x7ff0000000000000ll);
+  const float NANF = __int_as_float(0x7fc00000);
+  const abc_result& o = p.out;
+  for (uint64_t e = blockIdx.x; e < len; e += gridDim.x) {
+    const uint64_t v = p.list ? p.list[e] : e;
+    const float* y = p.tacs + v * p.L;
+    uint32_t cnt = 0;
+    float tK = __int_as_float(0x7f800000);
+    if (p.exact) {
+      cnt = p.n;
+      for (uint32_t a = threadIdx.x; a < Kp; a += kLT) {
+        cd[a] = a < cnt ? p.hd[v * p.n + a] : DINF;
+        ci[a] = a < cnt ? p.hidx[v * p.n + a] : 0xffffffffu;
+      }
+    } else {
+      const uint32_t S = p.nparts;
+      float B = __int_as_float(0x7f800000);
+      uint64_t total = 0;
+      for (uint32_t q = 0; q < S; ++q) total += p.heap_cnt[v * S + q];
+      if (p.tau_glob) {
+        B = __uint_as_float(p.tau_glob[v]);
+      } else if (p.heap_cnt[v] >= p.K) {  // flat mode: the root of the single heap is its maximum
+        B = __uint_as_float(uint32_t(p.heap[v * heap_stride(p.K) + kHeapOff] >> 32));
+      }
+      const bool complete = (total == p.N);
+      bool to_fb = p.force_fb || (!complete && !(B < __int_as_float(0x7f800000)));
+      if (!to_fb) {
+        if (threadIdx.x == 0) sc[0] = 0;
+        __syncthreads();
+        for (uint32_t q = 0; q < S; ++q) {
+          const uint32_t cq = p.heap_cnt[v * S + q];
+          const unsigned long long* h = p.heap + (v * S + q) * heap_stride(p.K) + kHeapOff;
+          for (uint32_t a = threadIdx.x; a < cq; a += kLT) {
+            const unsigned long long key = h[a];
+            if (__uint_as_float(uint32_t(key >> 32)) <= B) {
+              const uint32_t pos = atomicAdd(&sc[0], 1u);
+              if (pos < Kp) ci[pos] = uint32_t(key & 0xffffffffull);
+            }
+          }
+        }
+        __syncthreads();
+        cnt = sc[0];
+        to_fb = cnt > Kp || cnt < p.n;
+      }
+      if (to_fb) {
+        if (threadIdx.x == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+        __syncthreads();
+        continue;
+      }
+      for (uint32_t a = threadIdx.x; a < Kp; a += kLT) {
+        if (a < cnt) {
+          cd[a] = exact_distance_c(y, p.bank + uint64_t(ci[a]) * p.LS, p.w, p.L, p.dist);
+        } else {
+          cd[a] = DINF;
+          ci[a] = 0xffffffffu;
+        }
+      }
+      tK = complete ? __int_as_float(0x7f800000) : B;
+    }
+    __syncthreads();
+    {
+      uint32_t kp = 2;
+      while (kp < cnt) kp <<= 1;
+      cta_sort_pairs(cd, ci, kp < Kp ? kp : Kp);
+    }
+    if (!p.exact && tK < __int_as_float(0x7f800000)) {
+      double Y2 = 0.0, Y1 = 0.0;
+      for (uint32_t f = threadIdx.x; f < p.L; f += kLT) {
+        const double yv = __ldg(y + f), wv = __ldg(p.w + f);
+        Y2 += wv * yv * yv;
+        Y1 += wv * fabs(yv);
+      }
+      Y2 = cta_sum(Y2, red);
+      Y1 = cta_sum(Y1, red);
+      const double t64 = cd[p.n - 1];
+      const double err = p.eb.a * t64 + p.eb.b * sqrt(Y2 * t64) + p.eb.c * Y2 + p.eb.d * Y1;
+      if (!(double(tK) > t64 + err)) {
+        if (threadIdx.x == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+        __syncthreads();
+        continue;
+      }
+    }
+    // ---- K4: reduce the accepted (D, i)-sorted list ci[0..n) ----
+    const uint32_t n = p.n, M = p.prior.M;
+    for (uint32_t a = threadIdx.x; a < n; a += kLT) {
+      if (o.acc_idx) o.acc_idx[v * n + a] = ci[a];
+      if (o.acc_dist) o.acc_dist[v * n + a] = cd[a];
+    }
+    if (threadIdx.x < ABC_MAX_MODELS) sc[4 + threadIdx.x] = 0;
+    __syncthreads();
+    for (uint32_t a = threadIdx.x; a < n; a += kLT) atomicAdd(&sc[4 + model_index(p.prior, ci[a])], 1u);
+    __syncthreads();
+    uint32_t cntm[ABC_MAX_MODELS];
+    for (int m = 0; m < ABC_MAX_MODELS; ++m) cntm[m] = sc[4 + m];
+    int pref = 0;
+    for (uint32_t m = 1; m < M; ++m)
+      if (cntm[m] > cntm[pref]) pref = int(m);
+    if (threadIdx.x == 0) {
+      for (uint32_t m = 0; m < M; ++m) {
+        if (o.count) o.count[v * M + m] = cntm[m];
+        if (o.prob) o.prob[v * M + m] = float(double(cntm[m]) / double(n));
+      }
+      if (o.preferred) o.preferred[v] = pref;
+    }
+    const int kind = p.prior.m[pref].kind;
+    const uint32_t c = cntm[pref];
+    const bool tcm = kind <= ABC_2TCM_REV;
+    uint64_t* kv = reinterpret_cast<uint64_t*>(cd);  // the distances are written out: reuse as keys
+    __syncthreads();
+    for (uint32_t k = 0; k <= p.P; ++k) {  // column P = K_i
+      const bool is_ki = (k == p.P);
+      float mean = NANF, sd = NANF, q3[3] = {NANF, NANF, NANF};
+      const bool exists = c > 0 && (is_ki ? tcm : column_exists(kind, k));
+      if (exists) {
+        const uint32_t blk = (is_ki || k < 4) ? 0u : 1u;
+        double sum = 0.0;
+        for (uint32_t a = threadIdx.x; a < n; a += kLT) {
+          const uint32_t i = ci[a];
+          uint64_t key = ~0ull;  // other models sort last
+          if (model_index(p.prior, i) == pref) {
+            float th[ABC_MAX_P];
+            theta_block(p.prior, i, pref, blk, th);
+            const double x = is_ki ? double(th[0]) * double(th[2]) / (double(th[1]) + double(th[2])) : double(th[k]);
+            sum += x;
+            key = okey(x);
+          }
+          kv[a] = key;
+        }
+        const double mu = cta_sum(sum, red) / double(c);
+        double ss = 0.0;
+        for (uint32_t a = threadIdx.x; a < n; a += kLT)
+          if (kv[a] != ~0ull) {
+            const double x = okey_inv(kv[a]);
+            ss += (x - mu) * (x - mu);
+          }
+        ss = cta_sum(ss, red);
+        mean = float(mu);
+        sd = c >= 2 ? float(sqrt(ss / double(c - 1))) : NANF;
+        const double qs[3] = {0.025, 0.5, 0.975};
+        for (int t = 0; t < 3; ++t) {  // type 7: x[lo] + (h - lo)(x[lo + 1] - x[lo]), h = (c - 1) q
+          const double h = double(c - 1) * qs[t];
+          const uint32_t lo = uint32_t(floor(h));
+          const double xlo = okey_inv(cta_select(kv, n, lo, hist, sc + 8));
+          double qv = xlo;
+          if (lo + 1 < c) {
+            const double xhi = okey_inv(cta_select(kv, n, lo + 1, hist, sc + 8));
+            qv = xlo + (h - double(lo)) * (xhi - xlo);
+          }
+          q3[t] = float(qv);
+        }
+      }
+      if (threadIdx.x == 0) {
+        if (is_ki) {
+          if (o.ki_mean) o.ki_mean[v] = mean;
+          if (o.ki_sd) o.ki_sd[v] = sd;
+          if (o.ki_q) for (int t = 0; t < 3; ++t) o.ki_q[v * 3 + t] = q3[t];
+        } else {
+          if (o.mean) o.mean[v * p.P + k] = mean;
+          if (o.sd) o.sd[v * p.P + k] = sd;
+          if (o.q) for (int t = 0; t < 3; ++t) o.q[(v * p.P + k) * 3 + t] = q3[t];
+        }
+      }
+      __syncthreads();
+    }
+    (void)lane;
+  }
+}
+
 // ---- exact FP64 scan: thread per voxel, max-heap of (D64, i) of size n, prefix pruning ----
 __device__ __noinline__ double exact_push(double* hd, uint32_t* hi, uint32_t n, uint32_t& cnt, double D, uint32_t idx) {
   if (cnt < n) {
@@ -649,9 +931,31 @@ __global__ void response_envelope_kernel(const EnvelopeParams p, uint32_t np2, u
 
 }  // namespace
 
+size_t certify_large_smem(uint32_t Kp) { return size_t(Kp) * 12 + 256 * 4 + 16 * 4 + (kLT / 32) * 8; }
+
+uint32_t certify_candidates_pow2(const ReduceParams& p) {
+  return next_pow2(p.exact ? p.n : (p.K * p.nparts > p.n ? p.K * p.nparts : p.n));
+}
+
 cudaError_t launch_certify_reduce(const ReduceParams& p, cudaStream_t st) {
-  uint32_t Kp = next_pow2(p.exact ? p.n : (p.K * p.nparts > p.n ? p.K * p.nparts : p.n));
+  uint32_t Kp = certify_candidates_pow2(p);
   if (Kp < 32) Kp = 32;
+  if (Kp > kWarpCertifyMax) {  // large n: one CTA per voxel, candidates and sorts CTA-wide
+    if (Kp > kLargeMaxCand) return cudaErrorInvalidValue;
+    const size_t smem = certify_large_smem(Kp);
+    cudaError_t e = ensure_smem_attr((const void*)certify_large_kernel, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, certify_large_kernel, kLT, smem);
+    uint64_t blocks = uint64_t(nsm) * uint64_t(occ > 0 ? occ : 1);
+    if (blocks > p.J) blocks = p.J;
+    if (blocks == 0) blocks = 1;
+    certify_large_kernel<<<unsigned(blocks), kLT, smem, st>>>(p, Kp);
+    return cudaGetLastError();
+  }
   uint32_t np2 = next_pow2(p.n);
   if (np2 < 32) np2 = 32;
   size_t per_warp = size_t(Kp) * 12 + size_t(np2) * 8;

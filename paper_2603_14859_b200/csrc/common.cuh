@@ -368,6 +368,11 @@ struct ReduceParams {
   abc_result out;
 };
 cudaError_t launch_certify_reduce(const ReduceParams& p, cudaStream_t st);
+// Certification layouts: warp per voxel while the candidate set (a power of two) is <= kWarpCertifyMax,
+// else one CTA per voxel with up to kLargeMaxCand candidates in shared memory (196 KB).
+constexpr uint32_t kWarpCertifyMax = 2048;
+constexpr uint32_t kLargeMaxCand = 16384;
+constexpr uint32_t kMaxAccept = 15360;  // n_accept cap: n + n/16 slack <= kLargeMaxCand (one part)
 // K4 on given accepted lists (abc_reduce_accepted): the first p.n of n_acc indices per voxel.
 cudaError_t launch_reduce_list(const ReduceParams& p, const uint64_t* idx, uint32_t n_acc, int* bad, cudaStream_t st);
 

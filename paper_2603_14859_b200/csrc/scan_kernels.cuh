@@ -521,6 +521,20 @@ __device__ __forceinline__ void refresh_tau(const ScanParams& p, Voxels<LP, R>& 
   }
 }
 
+// Split refresh: issue the loads (early), apply them (late).
+template <int LP, int R>
+__device__ __forceinline__ void refresh_issue(const ScanParams& p, const Voxels<LP, R>& V, float (&g)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    g[r] = (!p.eps_mode && p.tau_glob && V.vox[r] < p.J) ? __uint_as_float(__ldcg(p.tau_glob + V.vox[r]))
+                                                          : __int_as_float(0x7f800000);
+}
+template <int LP, int R>
+__device__ __forceinline__ void refresh_apply(Voxels<LP, R>& V, const float (&g)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) V.tau[r] = fminf(V.tau[r], g[r]);
+}
+
 // Software-pipelined variant: apply the value loaded at the previous call, issue the next load.
 template <int LP, int R>
 __device__ __forceinline__ void refresh_tau_pipe(const ScanParams& p, Voxels<LP, R>& V, float (&gpend)[R]) {
@@ -734,15 +748,15 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
   uint32_t* wmask = reinterpret_cast<uint32_t*>(arrivals + NST);
   float* ybar = reinterpret_cast<float*>(wmask + NW);
   int* s_item = reinterpret_cast<int*>(ybar + NW * LP);
-  uint32_t* horder = reinterpret_cast<uint32_t*>(
-      (reinterpret_cast<uintptr_t>(s_item + 4) + 15) & ~uintptr_t(15));  // [kHyperSort] hyper-tile order
-  uint32_t* sorder = horder + kHyperSort;                                  // [kHyperSort] super-tile order
+  // 16-B aligned sub-buffers, addressed as smem_raw + offset (so the compiler keeps the shared
+  // address space and emits LDS, not generic loads, for the prefetched boxes)
+  auto align16 = [&](const void* q) { return (size_t(static_cast<const unsigned char*>(q) - smem_raw) + 15) & ~size_t(15); };
+  uint32_t* horder = reinterpret_cast<uint32_t*>(smem_raw + align16(s_item + 4));  // [kHyperSort] hyper-tile order
+  uint32_t* sorder = horder + kHyperSort;                                            // [kHyperSort] super-tile order
   constexpr size_t BXF = Shape<LP>::BOXB_FLOATS;
-  float* bbuf = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(sorder + kHyperSort) + 15) & ~uintptr_t(15));  // [2][BXF]
-  uint64_t* bbar = reinterpret_cast<uint64_t*>(bbuf + 2 * BXF);                  // [2]
-  unsigned long long* htop = reinterpret_cast<unsigned long long*>(
-      (reinterpret_cast<uintptr_t>(bbar + 2) + 15) & ~uintptr_t(15));  // [R][NT][9] heap tops
+  float* bbuf = reinterpret_cast<float*>(smem_raw + align16(sorder + kHyperSort));  // [2][BXF]
+  uint64_t* bbar = reinterpret_cast<uint64_t*>(bbuf + 2 * BXF);                    // [2]
+  unsigned long long* htop = reinterpret_cast<unsigned long long*>(smem_raw + align16(bbar + 2));  // [R][NT][9]
   unsigned long long* htop_t = VPET_SHEAP ? htop + threadIdx.x * 9 : nullptr;
   const uint32_t htop_s = smem_u32(htop) + uint32_t(threadIdx.x) * 72u;  // this thread's heap tops (bytes)
 
@@ -915,10 +929,15 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
         const int st = int(g % NST);
         // every warp observes every phase of the ring (parity waits are only unambiguous when no
         // phase is skipped), then only the warps whose lanes can improve evaluate the tile
+        // VPET_TREFRESH 3: the shared-threshold load is issued before the ring wait, so its L2 round
+        // trip overlaps the wait (the value is as fresh as mode 2's up to the wait time)
+        float gnow[R];
+        if (VPET_TREFRESH == 3 && ((mym >> b) & 1u)) refresh_issue<LP, R>(p, V, gnow);
         mbar_wait(&full[st], (g / NST) & 1u);
         if ((mym >> b) & 1u) {
           if (VPET_TREFRESH == 1) refresh_tau_pipe<LP, R>(p, V, gpend);
           if (VPET_TREFRESH == 2) refresh_tau<LP, R>(p, V);
+          if (VPET_TREFRESH == 3) refresh_apply<LP, R>(V, gnow);
           const float* sb = stage + size_t(st) * Shape<LP>::STAGE_FLOATS;
           const uint32_t* si = sidx + st * T;
           const uint64_t rem = N - t * T;

@@ -52,7 +52,7 @@ def test_init_rejects_bad_configs_before_touching_a_device():
                      dict(kind="MRTM", n_draws=10, lo=[0.5] * 7, hi=[1.0] * 7)], n_accept=1),            # mixed families
         dict(models=[dict(kind="2TCM_REV", n_draws=10, lo=lo, hi=hi)], accept="EPS", epsilon=-1.0),
         dict(models=[dict(kind="2TCM_REV", n_draws=2 ** 32, lo=lo, hi=hi)], n_accept=1),
-        dict(models=[dict(kind="2TCM_REV", n_draws=10000, lo=lo, hi=hi)], n_accept=5000),   # n > 4096
+        dict(models=[dict(kind="2TCM_REV", n_draws=100000, lo=lo, hi=hi)], n_accept=15361),  # n > 15360
     ]
     for kw in bad:
         with pytest.raises(AbcError) as e:

@@ -331,3 +331,17 @@ def test_epsilon_calibrated_from_pilot(tb_small):
     assert 0.5 <= frac <= 0.5 + 2.0 / p.J, frac
     below = cnt < 60
     np.testing.assert_array_equal(cnt[below], np.sum(g["acc_dist"][below] <= eps, axis=1))
+
+
+@pytest.mark.parametrize("N,n,flags", [(40_000, 3000, 0), (20_000, 9000, 0), (40_000, 3000, 0x80), (16_000, 5000, 0x20)])
+def test_large_n_cta_certification(tb_small, N, n, flags):
+    """n beyond the warp layout (candidate sets > 2048): one CTA per voxel certifies and reduces
+    (CTA bitonic sort of up to 16384 (D64, i) pairs, radix-select quantiles); n = 9000 also takes the
+    single-part scan.  Forced fallback (0x80) and the flat scan (0x20) at large n too."""
+    half = N // 2
+    models = [dict(m, n_draws=(half if k == 0 else N - half)) for k, m in enumerate(tb_small.ctx_kwargs["models"])]
+    p = tb_small.replace(models=models, n_accept=n).subset(np.arange(48))
+    g, _ = run_gpu(p, flags=flags)
+    o, _ = run_oracle(p)
+    rep = compare(g, o)
+    assert rep["matched"] >= p.J - 2

@@ -1,4 +1,8 @@
-"""Build tuning variants of libvpetabc.so into tune/ (compile-time VPET_TILE / VPET_SUPER / VPET_CH)."""
+"""Build tuning variants of libvpetabc.so (compile-time VPET_* knobs) into paper_2603_14859_b200/_variants/
+(git-ignored *.so, but shipped to the GPU box by gpurun); select one with VPET_LIB=<path>.
+
+python tools/build_variants.py base acc2 ...
+"""
 import concurrent.futures as cf
 import os
 import sys
@@ -8,12 +12,14 @@ from paper_2603_14859_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": (),
+    "acc2": ("VPET_ACC2=1",),
+    "tr3": ("VPET_TREFRESH=3",),
+    "tr3acc2": ("VPET_TREFRESH=3", "VPET_ACC2=1"),
     "npc3": ("VPET_NPC=3",),
     "npc5": ("VPET_NPC=5",),
-    "npc6": ("VPET_NPC=6",),
 }
 names = sys.argv[1:] or list(VARIANTS)
-root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tune")
+root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2603_14859_b200", "_variants")
 os.makedirs(root, exist_ok=True)
 with cf.ThreadPoolExecutor(max_workers=2) as ex:
     futs = {n: ex.submit(B.build, True, False, os.path.join(root, f"libvpetabc_{n}.so"), VARIANTS[n] or ("VPET_BASE=1",))

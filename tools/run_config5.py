@@ -31,7 +31,7 @@ rows = []
 for N in [int(x) for x in a.draws.split(",")]:
     for p in [float(x) for x in a.p.split(",")]:
         n = int(np.floor(N * p))
-        if n < 1 or n > 4096:
+        if n < 1 or n > 15360:
             continue
         models = [dict(m, n_draws=N // 2) for m in base.ctx_kwargs["models"]]
         prob = base.replace(models=models, n_accept=n)
