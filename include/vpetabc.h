@@ -94,8 +94,8 @@ typedef enum { ABC_INPUT_PWL = 0, ABC_INPUT_FENG = 1 } abc_input_kind;
                                     L <= 48, n <= 2032, else ABC_E_UNSUPPORTED).  Same certified results;
                                     evaluates every pair (SURVEY.md §8f-1, A/B comparison) */
 #define ABC_FLAG_FORCE_FALLBACK 0x80u /* test hook: certification rejects every voxel, so every
-                                    voxel is re-run by the exact FP64 scan (the uncertified-voxel
-                                    path of DESIGN.md §3); results must be unchanged */
+                                    voxel takes the uncertified-voxel path (seeded FP64 collector,
+                                    DESIGN.md §3); results must be unchanged */
 
 /* abc_run_voxels ptr_flags */
 #define ABC_PTR_TACS_DEVICE 0x1u /* tacs is a device pointer on ctx's device */
@@ -150,6 +150,8 @@ typedef struct abc_stats {
   uint64_t n_voxels;
   uint64_t n_draws;
   uint64_t n_fallback;        /* voxels whose FP32 pass could not be certified (re-run exactly) */
+  uint64_t n_fallback_exact;  /* of these, voxels re-run by the exact heap scan (the others by the
+                                 seeded GPU-wide collector) */
   uint64_t frame_updates;     /* executed FP32 frame updates of draw evaluations (ABC_FLAG_COUNT_WORK) */
   uint64_t bound_updates;     /* executed FP32 frame updates of (super-)tile lower bounds (idem) */
   uint32_t lp;                /* padded frame count of the FP32 pass */

@@ -54,7 +54,8 @@ class Result(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("gpu_launches", C.c_uint32), ("n_voxels", C.c_uint64),
-                ("n_draws", C.c_uint64), ("n_fallback", C.c_uint64), ("frame_updates", C.c_uint64),
+                ("n_draws", C.c_uint64), ("n_fallback", C.c_uint64), ("n_fallback_exact", C.c_uint64),
+                ("frame_updates", C.c_uint64),
                 ("bound_updates", C.c_uint64),
                 ("lp", C.c_uint32), ("heap_k", C.c_uint32),
                 ("ms_h2d", C.c_double), ("ms_bank", C.c_double), ("ms_order", C.c_double),

@@ -86,6 +86,7 @@ struct abc_ctx {
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
   DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, hbounds, tau_glob, queue;
   DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp, item_log;
+  DevBuf fb_tau, cl_d, cl_i, cl_cnt, fb2_list, fb2_len;  // fallback tiers (certify.cu)
   DevBuf dBt, dS2, dAt, dY2;  // ABC_FLAG_DENSE_TC operands (dense_tc.cu)
   DevBuf env_idx, env_t, env_q;  // abc_response_envelope staging
   DevBuf proj;                   // [N][kNPC] bank projections (order stage)
@@ -563,8 +564,13 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   uint32_t K = 0;
   if (!eps) {
     // dense mode: a wider candidate band, since its dot-form error bound is ~1e-4 of ||y||^2 (vs ~u D)
-    uint64_t k = dense ? 4 * uint64_t(n) + 64 : uint64_t(n) + std::max<uint64_t>(8, n / 16);
-    k = (k + 7) & ~7ull;
+    // FP32 pass: K = n + slack candidates per part.  The K-th smallest D32 is the pruning threshold, so
+    // a small slack prunes harder; the slack (>= 1) only has to keep D_(K) above D_(n) + err for the
+    // certification, which 8 draws do with a wide margin at the paper's noise levels.
+    static const uint64_t slack = getenv("VPET_KSLACK") ? uint64_t(std::max(1, atoi(getenv("VPET_KSLACK")))) : 8;  // tuning knob
+    uint64_t k = dense ? 4 * uint64_t(n) + 64 : uint64_t(n) + std::max<uint64_t>(slack, n / 16);
+    if (dense) k = (k + 7) & ~7ull;
+    if (getenv("VPET_KROUND")) k = (k + 7) & ~7ull;  // tuning knob: round-1 behaviour
     K = uint32_t(std::min<uint64_t>(k, N));
   }
   S.lp = LP;
@@ -615,7 +621,19 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (tree) need += N * (8 + 8 + 4 + 4 + 4 + 4 * kNPC) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper + nhyper);
   if (tree) need += 24 * J + vsort_tmp;
   if (!eps) need += (size_t(8) * heap_stride(std::max<uint32_t>(K, 1)) + 4) * J * nparts + 4 * J;  // heaps
-  need += size_t(12) * J * (n ? n : 1);                  // exact heaps (fallback)
+  need += size_t(12) * J * (n ? n : 1);                  // exact heaps (last-resort fallback)
+  // fallback collector lists: cl_cap (the certification capacity) entries for up to cl_voxels voxels
+  uint32_t cl_cap = 32, cl_voxels = 0;
+  if (!eps && !exact) {
+    ReduceParams tmp{};
+    tmp.K = K;
+    tmp.nparts = dense ? 2u : ((tree) ? nparts : 1u);
+    tmp.n = n;
+    cl_cap = certify_capacity(tmp);
+    const uint64_t by_mem = (uint64_t(256) << 20) / (12ull * cl_cap);
+    cl_voxels = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(J, by_mem)));
+    need += size_t(12) * cl_cap * cl_voxels + 4 * size_t(cl_voxels) + 12 * J + 16;
+  }
   if (eps) need += sizeof(Fix128) * J * nparts * M * MOMW;
   if (host_tacs) need += sizeof(float) * J * L;
   need += out_bytes + 8 * J + (64u << 20);
@@ -675,6 +693,14 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   }
   CK(ctx->fb_list.ensure(4 * J));
   CK(ctx->fb_len.ensure(16));
+  if (cl_voxels) {
+    CK(ctx->fb_tau.ensure(8 * J));
+    CK(ctx->cl_d.ensure(size_t(8) * cl_cap * cl_voxels));
+    CK(ctx->cl_i.ensure(size_t(4) * cl_cap * cl_voxels));
+    CK(ctx->cl_cnt.ensure(size_t(4) * cl_voxels));
+    CK(ctx->fb2_list.ensure(4 * J));
+    CK(ctx->fb2_len.ensure(16));
+  }
   CK(ctx->work.ensure(16));
   CK(ctx->flag.ensure(16));
   if (host_tacs) CK(ctx->tacs.ensure(sizeof(float) * J * L));
@@ -726,6 +752,10 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   rec(EV_H2D);
   CK(cudaMemsetAsync(ctx->flag.p, 0, 16, st));
   CK(cudaMemsetAsync(ctx->fb_len.p, 0, 16, st));
+  if (cl_voxels) {
+    CK(cudaMemsetAsync(ctx->fb2_len.p, 0, 16, st));
+    CK(cudaMemsetAsync(ctx->cl_cnt.p, 0, size_t(4) * cl_voxels, st));
+  }
   CK(cudaMemsetAsync(ctx->work.p, 0, 16, st));
   bool joined = false;
   auto join_tacs = [&]() -> cudaError_t {  // before the first kernel that reads the TACs
@@ -917,6 +947,16 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   rp.fb_len = ctx->fb_len.as<uint32_t>();
   rp.force_fb = (ctx->cfg.flags & ABC_FLAG_FORCE_FALLBACK) ? 1 : 0;
   rp.bad = ctx->flag.as<int>();
+  if (cl_voxels) {
+    rp.fb_tau = ctx->fb_tau.as<double>();
+    rp.cl_d = ctx->cl_d.as<double>();
+    rp.cl_i = ctx->cl_i.as<uint32_t>();
+    rp.cl_cnt = ctx->cl_cnt.as<uint32_t>();
+    rp.cl_cap = cl_cap;
+    rp.cl_voxels = cl_voxels;
+    rp.fb2_list = ctx->fb2_list.as<uint32_t>();
+    rp.fb2_len = ctx->fb2_len.as<uint32_t>();
+  }
   rp.out = dout;
 
   ExactParams xp{};
@@ -955,16 +995,49 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(launch_certify_reduce(rp, st));
     ++launches;
     rec(EV_CERT);
-    // uncertified voxels: exact scan + reduce over the device-side list (no host sync)
-    xp.list = ctx->fb_list.as<uint32_t>();
-    xp.list_len = ctx->fb_len.as<uint32_t>();
+    // uncertified voxels (device-side list, no host sync).  Tier 2: every draw with D64 <= the seed
+    // (the n-th FP64 distance among the voxel's candidates, >= tau64) is collected by a GPU-wide
+    // FP64 scan, then sorted and reduced.  Tier 3 (seed unknown or list overflow): exact heap scan.
+    ReduceParams rc = rp;
+    rc.force_fb = 0;
+    if (cl_voxels) {
+      CollectParams cp{};
+      cp.bank = ctx->bank.as<float>();
+      cp.N = N;
+      cp.L = L;
+      cp.LS = LS;
+      cp.tacs = d_tacs;
+      cp.w = ctx->d_w.as<float>();
+      cp.dist = ctx->cfg.distance;
+      cp.list = ctx->fb_list.as<uint32_t>();
+      cp.list_len = ctx->fb_len.as<uint32_t>();
+      cp.tau = ctx->fb_tau.as<double>();
+      cp.cap_voxels = cl_voxels;
+      cp.cap = cl_cap;
+      cp.nchunk = 2048;
+      cp.cnt = ctx->cl_cnt.as<uint32_t>();
+      cp.cd = ctx->cl_d.as<double>();
+      cp.ci = ctx->cl_i.as<uint32_t>();
+      cp.bad = ctx->flag.as<int>();
+      launch_fallback_collect(cp, st);
+      rc.exact = 2;
+      rc.list = ctx->fb_list.as<uint32_t>();
+      rc.list_len = ctx->fb_len.as<uint32_t>();
+      rc.fb_list = nullptr;
+      CK(launch_certify_reduce(rc, st));
+      launches += 2;
+      xp.list = ctx->fb2_list.as<uint32_t>();
+      xp.list_len = ctx->fb2_len.as<uint32_t>();
+    } else {
+      xp.list = ctx->fb_list.as<uint32_t>();
+      xp.list_len = ctx->fb_len.as<uint32_t>();
+    }
     launch_exact_scan(xp, st);
-    ReduceParams rx = rp;
+    ReduceParams rx = rc;
     rx.exact = 1;
     rx.list = xp.list;
     rx.list_len = xp.list_len;
     rx.fb_list = nullptr;
-    rx.force_fb = 0;
     CK(launch_certify_reduce(rx, st));
     launches += 2;
     rec(EV_FB);
@@ -979,16 +1052,18 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   rec(EV_D2H);
   h2 = hnow();
   int h_flag = 0;
-  uint32_t h_fb = 0;
+  uint32_t h_fb = 0, h_fb2 = 0;
   unsigned long long h_work[2] = {0, 0};
   CK(cudaMemcpyAsync(&h_flag, ctx->flag.p, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&h_fb, ctx->fb_len.p, 4, cudaMemcpyDeviceToHost, st));
+  if (cl_voxels && !exact && !eps) CK(cudaMemcpyAsync(&h_fb2, ctx->fb2_len.p, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h_work, ctx->work.p, 16, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   h3 = hnow();
   if (host_dbg) fprintf(stderr, "host: tables %.3f plan+alloc %.3f prep %.3f enqueue %.3f wait %.3f ms\n", h_tab - h0, h_alloc - h_tab, h1 - h_alloc, h2 - h1, h3 - h2);
   S.gpu_launches = launches;
   S.n_fallback = h_fb;
+  S.n_fallback_exact = cl_voxels ? h_fb2 : h_fb;
   S.frame_updates = h_work[0];
   S.bound_updates = h_work[1];
   if (timing) {
@@ -1226,7 +1301,8 @@ void abc_destroy(abc_ctx* ctx) {
                      &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob,
                      &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp, &ctx->item_log,
                      &ctx->dBt, &ctx->dS2, &ctx->dAt, &ctx->dY2,
-                     &ctx->env_idx, &ctx->env_t, &ctx->env_q, &ctx->proj, &ctx->pat_ab};
+                     &ctx->env_idx, &ctx->env_t, &ctx->env_q, &ctx->proj, &ctx->pat_ab,
+                     &ctx->fb_tau, &ctx->cl_d, &ctx->cl_i, &ctx->cl_cnt, &ctx->fb2_list, &ctx->fb2_len};
   for (DevBuf* b : bufs2) b->release();
   DevBuf* bufs[] = {&ctx->d_finv, &ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,

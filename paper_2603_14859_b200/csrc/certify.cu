@@ -33,6 +33,14 @@ __device__ __forceinline__ bool pair_gt(double a, uint32_t ia, double b, uint32_
   return a > b || (a == b && ia > ib);
 }
 
+// Append voxel v to the fallback list with the seed threshold tau (see ReduceParams).
+__device__ __forceinline__ void push_fb(const ReduceParams& p, uint32_t v, double tau) {
+  const uint32_t pos = atomicAdd(p.fb_len, 1u);
+  p.fb_list[pos] = v;
+  if (p.fb_tau) p.fb_tau[pos] = tau;
+}
+__device__ __forceinline__ void push_fb2(const ReduceParams& p, uint32_t v) { p.fb2_list[atomicAdd(p.fb2_len, 1u)] = v; }
+
 // bitonic sort of (key, idx) pairs, ascending, n2 a power of two, one warp
 __device__ void warp_sort_pairs(double* key, uint32_t* idx, uint32_t n2, int lane) {
   for (uint32_t size = 2; size <= n2; size <<= 1) {
@@ -309,7 +317,17 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
     const float* y = p.tacs + v * p.L;
     uint32_t cnt;
     float tK = __int_as_float(0x7f800000);
-    if (p.exact) {
+    if (p.exact == 2) {  // the draws with D64 <= fb_tau collected for this fallback entry
+      cnt = e < p.cl_voxels ? p.cl_cnt[e] : 0xffffffffu;
+      if (!(p.fb_tau[e] < DINF) || cnt > p.cl_cap || cnt > Kp || cnt < p.n) {
+        if (lane == 0) push_fb2(p, uint32_t(v));
+        continue;
+      }
+      for (uint32_t a = lane; a < Kp; a += 32) {
+        cd[a] = a < cnt ? p.cl_d[e * p.cl_cap + a] : DINF;
+        ci[a] = a < cnt ? p.cl_i[e * p.cl_cap + a] : 0xffffffffu;
+      }
+    } else if (p.exact) {
       cnt = p.n;
       for (uint32_t a = lane; a < Kp; a += 32) {
         cd[a] = a < cnt ? p.hd[v * p.n + a] : DINF;
@@ -332,13 +350,9 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
         for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
         B = tmax;
       }
-      if (p.force_fb) {  // ABC_FLAG_FORCE_FALLBACK: every voxel takes the exact path (test hook)
-        if (lane == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
-        continue;
-      }
       const bool complete = (total == p.N);  // every draw was kept: nothing excluded
       if (!complete && !(B < __int_as_float(0x7f800000))) {  // no finite bound (non-finite D32s)
-        if (lane == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+        if (lane == 0) push_fb(p, uint32_t(v), DINF);
         continue;
       }
       uint32_t nc = 0;  // warp-uniform candidate count
@@ -358,7 +372,7 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
         }
       }
       if (nc > Kp || nc < p.n) {  // capacity (or a degenerate bound): exact path
-        if (lane == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+        if (lane == 0) push_fb(p, uint32_t(v), DINF);
         continue;
       }
       __syncwarp();
@@ -379,7 +393,7 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
       while (kp < cnt) kp <<= 1;
       warp_sort_any(cd, ci, kp < Kp ? kp : Kp, lane);
     }
-    if (!p.exact && tK < __int_as_float(0x7f800000)) {
+    if (!p.exact && (tK < __int_as_float(0x7f800000) || p.force_fb)) {
       double Y2 = 0.0, Y1 = 0.0;
       for (uint32_t f = lane; f < p.L; f += 32) {
         double yv = __ldg(y + f), wv = __ldg(p.w + f);
@@ -390,9 +404,9 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
       Y1 = warp_sum(Y1);
       double t64 = cd[p.n - 1];
       double err = p.eb.a * t64 + p.eb.b * sqrt(Y2 * t64) + p.eb.c * Y2 + p.eb.d * Y1;
-      bool ok = double(tK) > t64 + err;
-      if (!ok) {
-        if (lane == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+      bool ok = !p.force_fb && double(tK) > t64 + err;
+      if (!ok) {  // t64 >= tau64: every accepted draw has D64 <= t64 (the collector's seed)
+        if (lane == 0) push_fb(p, uint32_t(v), t64);
         continue;
       }
     }
@@ -404,20 +418,11 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
 // =============================================================================================
 // Large-n certification + reduction (K3/K4 for n up to kMaxAccept): one CTA of kLT threads per
 // voxel, candidates in shared memory (up to kLargeMaxCand (D64, i) pairs = 196 KB), a CTA-wide
-// bitonic sort of the candidates by (D64, i), and per-column type-7 quantiles by CTA radix select
-// (8-bit digits of order-preserving 64-bit keys) instead of sorts.  Same arithmetic and same
+// bitonic sort of the candidates by (D64, i), and a CTA-wide sort of each column's values for the
+// type-7 quantiles.  Same arithmetic and same
 // certification test as the warp path (certify_reduce_kernel); only the parallel layout differs.
 // =============================================================================================
 constexpr int kLT = 512;
-
-__device__ __forceinline__ uint64_t okey(double x) {  // order-preserving map of an FP64 value
-  const uint64_t u = uint64_t(__double_as_longlong(x));
-  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double okey_inv(uint64_t k) {
-  const uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-  return __longlong_as_double((long long)u);
-}
 
 // Ascending bitonic sort of n2 (power of two) (key, idx) pairs by (key, idx), whole CTA.
 __device__ void cta_sort_pairs(double* key, uint32_t* idx, uint32_t n2) {
@@ -438,45 +443,21 @@ __device__ void cta_sort_pairs(double* key, uint32_t* idx, uint32_t n2) {
   }
 }
 
-// Value of rank r (0-based) among kv[0..c) (uint64 keys), whole CTA; hist: 256 words, bc: 2 words.
-__device__ uint64_t cta_select(const uint64_t* kv, uint32_t c, uint32_t r, uint32_t* hist, uint32_t* bc) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t prefix = 0, decided = 0;
-  for (int shift = 56; shift >= 0; shift -= 8) {
-    for (uint32_t b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
-    __syncthreads();
-    for (uint32_t a = threadIdx.x; a < c; a += blockDim.x) {
-      const uint64_t k = kv[a];
-      if ((k & decided) == prefix) atomicAdd(&hist[(k >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t h[8], s = 0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) { h[q] = hist[lane * 8 + q]; s += h[q]; }
-      uint32_t inc = s;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
-      }
-      const uint32_t exc = inc - s;
-      if (exc <= r && r < inc) {
-        uint32_t acc = exc;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (r < acc + h[q]) { bc[0] = uint32_t(lane * 8 + q); bc[1] = r - acc; break; }
-          acc += h[q];
+// Ascending bitonic sort of n2 (power of two) doubles, whole CTA.
+__device__ void cta_sort_keys(double* key, uint32_t n2) {
+  for (uint32_t size = 2; size <= n2; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t t = threadIdx.x; t < n2 / 2; t += blockDim.x) {
+        const uint32_t i = 2 * t - (t & (stride - 1)), j = i + stride;
+        const double a = key[i], b = key[j];
+        if ((a > b) == ((i & size) == 0)) {
+          key[i] = b;
+          key[j] = a;
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
-    prefix |= uint64_t(bc[0]) << shift;
-    decided |= uint64_t(255) << shift;
-    r = bc[1];
-    __syncthreads();
   }
-  return prefix;
 }
 
 __device__ __forceinline__ double cta_sum(double x, double* red) {
@@ -505,12 +486,11 @@ __device__ __forceinline__ void theta_block(const PriorDev& pr, uint64_t i, int 
   if (blk == 1 && md.kind >= ABC_MRTM) th[5] = __fadd_rn(th[4], th[5]);
 }
 
-__global__ void __launch_bounds__(kLT, 1) certify_large_kernel(const ReduceParams p, uint32_t Kp) {
+__global__ void __launch_bounds__(kLT, 2) certify_large_kernel(const ReduceParams p, uint32_t Kp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* cd = reinterpret_cast<double*>(smem_raw);          // [Kp] D64 (later: uint64 value keys)
   uint32_t* ci = reinterpret_cast<uint32_t*>(cd + Kp);       // [Kp] draw indices
-  uint32_t* hist = ci + Kp;                                  // [256]
-  uint32_t* sc = hist + 256;                                 // [16] counters / broadcasts
+  uint32_t* sc = ci + Kp;                                    // [16] counters / broadcasts
   double* red = reinterpret_cast<double*>(sc + 16);          // [kLT / 32]
   if (p.bad && *p.bad) return;
   const int lane = threadIdx.x & 31;
@@ -523,7 +503,18 @@ __global__ void __launch_bounds__(kLT, 1) certify_large_kernel(const ReduceParam
     const float* y = p.tacs + v * p.L;
     uint32_t cnt = 0;
     float tK = __int_as_float(0x7f800000);
-    if (p.exact) {
+    if (p.exact == 2) {  // the draws with D64 <= fb_tau collected for this fallback entry
+      cnt = e < p.cl_voxels ? p.cl_cnt[e] : 0xffffffffu;
+      if (!(p.fb_tau[e] < DINF) || cnt > p.cl_cap || cnt > Kp || cnt < p.n) {
+        if (threadIdx.x == 0) push_fb2(p, uint32_t(v));
+        __syncthreads();
+        continue;
+      }
+      for (uint32_t a = threadIdx.x; a < Kp; a += kLT) {
+        cd[a] = a < cnt ? p.cl_d[e * p.cl_cap + a] : DINF;
+        ci[a] = a < cnt ? p.cl_i[e * p.cl_cap + a] : 0xffffffffu;
+      }
+    } else if (p.exact) {
       cnt = p.n;
       for (uint32_t a = threadIdx.x; a < Kp; a += kLT) {
         cd[a] = a < cnt ? p.hd[v * p.n + a] : DINF;
@@ -540,7 +531,7 @@ __global__ void __launch_bounds__(kLT, 1) certify_large_kernel(const ReduceParam
         B = __uint_as_float(uint32_t(p.heap[v * heap_stride(p.K) + kHeapOff] >> 32));
       }
       const bool complete = (total == p.N);
-      bool to_fb = p.force_fb || (!complete && !(B < __int_as_float(0x7f800000)));
+      bool to_fb = !complete && !(B < __int_as_float(0x7f800000));
       if (!to_fb) {
         if (threadIdx.x == 0) sc[0] = 0;
         __syncthreads();
@@ -560,7 +551,7 @@ __global__ void __launch_bounds__(kLT, 1) certify_large_kernel(const ReduceParam
         to_fb = cnt > Kp || cnt < p.n;
       }
       if (to_fb) {
-        if (threadIdx.x == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+        if (threadIdx.x == 0) push_fb(p, uint32_t(v), DINF);
         __syncthreads();
         continue;
       }
@@ -580,7 +571,7 @@ __global__ void __launch_bounds__(kLT, 1) certify_large_kernel(const ReduceParam
       while (kp < cnt) kp <<= 1;
       cta_sort_pairs(cd, ci, kp < Kp ? kp : Kp);
     }
-    if (!p.exact && tK < __int_as_float(0x7f800000)) {
+    if (!p.exact && (tK < __int_as_float(0x7f800000) || p.force_fb)) {
       double Y2 = 0.0, Y1 = 0.0;
       for (uint32_t f = threadIdx.x; f < p.L; f += kLT) {
         const double yv = __ldg(y + f), wv = __ldg(p.w + f);
@@ -591,8 +582,8 @@ __global__ void __launch_bounds__(kLT, 1) certify_large_kernel(const ReduceParam
       Y1 = cta_sum(Y1, red);
       const double t64 = cd[p.n - 1];
       const double err = p.eb.a * t64 + p.eb.b * sqrt(Y2 * t64) + p.eb.c * Y2 + p.eb.d * Y1;
-      if (!(double(tK) > t64 + err)) {
-        if (threadIdx.x == 0) p.fb_list[atomicAdd(p.fb_len, 1u)] = uint32_t(v);
+      if (p.force_fb || !(double(tK) > t64 + err)) {
+        if (threadIdx.x == 0) push_fb(p, uint32_t(v), t64);
         __syncthreads();
         continue;
       }
@@ -622,7 +613,9 @@ __global__ void __launch_bounds__(kLT, 1) certify_large_kernel(const ReduceParam
     const int kind = p.prior.m[pref].kind;
     const uint32_t c = cntm[pref];
     const bool tcm = kind <= ABC_2TCM_REV;
-    uint64_t* kv = reinterpret_cast<uint64_t*>(cd);  // the distances are written out: reuse as keys
+    double* xv = cd;  // the distances are written out: reuse the space for the column values
+    uint32_t np2 = 2;
+    while (np2 < n) np2 <<= 1;
     __syncthreads();
     for (uint32_t k = 0; k <= p.P; ++k) {  // column P = K_i
       const bool is_ki = (k == p.P);
@@ -631,40 +624,30 @@ __global__ void __launch_bounds__(kLT, 1) certify_large_kernel(const ReduceParam
       if (exists) {
         const uint32_t blk = (is_ki || k < 4) ? 0u : 1u;
         double sum = 0.0;
-        for (uint32_t a = threadIdx.x; a < n; a += kLT) {
-          const uint32_t i = ci[a];
-          uint64_t key = ~0ull;  // other models sort last
-          if (model_index(p.prior, i) == pref) {
-            float th[ABC_MAX_P];
-            theta_block(p.prior, i, pref, blk, th);
-            const double x = is_ki ? double(th[0]) * double(th[2]) / (double(th[1]) + double(th[2])) : double(th[k]);
-            sum += x;
-            key = okey(x);
+        for (uint32_t a = threadIdx.x; a < np2; a += kLT) {
+          double x = DINF;  // other models (and padding) sort last
+          if (a < n) {
+            const uint32_t i = ci[a];
+            if (model_index(p.prior, i) == pref) {
+              float th[ABC_MAX_P];
+              theta_block(p.prior, i, pref, blk, th);
+              x = is_ki ? double(th[0]) * double(th[2]) / (double(th[1]) + double(th[2])) : double(th[k]);
+              sum += x;
+            }
           }
-          kv[a] = key;
+          xv[a] = x;
         }
         const double mu = cta_sum(sum, red) / double(c);
         double ss = 0.0;
         for (uint32_t a = threadIdx.x; a < n; a += kLT)
-          if (kv[a] != ~0ull) {
-            const double x = okey_inv(kv[a]);
-            ss += (x - mu) * (x - mu);
-          }
+          if (xv[a] != DINF) ss += (xv[a] - mu) * (xv[a] - mu);
         ss = cta_sum(ss, red);
         mean = float(mu);
         sd = c >= 2 ? float(sqrt(ss / double(c - 1))) : NANF;
-        const double qs[3] = {0.025, 0.5, 0.975};
-        for (int t = 0; t < 3; ++t) {  // type 7: x[lo] + (h - lo)(x[lo + 1] - x[lo]), h = (c - 1) q
-          const double h = double(c - 1) * qs[t];
-          const uint32_t lo = uint32_t(floor(h));
-          const double xlo = okey_inv(cta_select(kv, n, lo, hist, sc + 8));
-          double qv = xlo;
-          if (lo + 1 < c) {
-            const double xhi = okey_inv(cta_select(kv, n, lo + 1, hist, sc + 8));
-            qv = xlo + (h - double(lo)) * (xhi - xlo);
-          }
-          q3[t] = float(qv);
-        }
+        cta_sort_keys(xv, np2);
+        q3[0] = float(quantile7(xv, c, 0.025));
+        q3[1] = float(quantile7(xv, c, 0.5));
+        q3[2] = float(quantile7(xv, c, 0.975));
       }
       if (threadIdx.x == 0) {
         if (is_ki) {
@@ -931,10 +914,56 @@ __global__ void response_envelope_kernel(const EnvelopeParams p, uint32_t np2, u
 
 }  // namespace
 
-size_t certify_large_smem(uint32_t Kp) { return size_t(Kp) * 12 + 256 * 4 + 16 * 4 + (kLT / 32) * 8; }
+size_t certify_large_smem(uint32_t Kp) { return size_t(Kp) * 12 + 16 * 4 + (kLT / 32) * 8; }
 
 uint32_t certify_candidates_pow2(const ReduceParams& p) {
+  if (p.exact == 2) return p.cl_cap;  // collected fallback lists (a power of two)
   return next_pow2(p.exact ? p.n : (p.K * p.nparts > p.n ? p.K * p.nparts : p.n));
+}
+
+uint32_t certify_capacity(const ReduceParams& p) {
+  const uint32_t Kp = certify_candidates_pow2(p);
+  return Kp < 32 ? 32 : Kp;
+}
+
+// Fallback collector (see CollectParams): warp item w = (entry e, chunk c) scans draws
+// [N c / nchunk, N (c + 1) / nchunk) lane-strided, FP64 in acquisition order with prefix pruning
+// against the fixed seed tau[e] (prefix sums only grow: a prefix > tau means D > tau).
+__global__ void __launch_bounds__(256) fallback_collect_kernel(const CollectParams p) {
+  if (p.bad && *p.bad) return;
+  const uint32_t len = min(*p.list_len, p.cap_voxels);
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x >> 5);
+  const uint64_t items = uint64_t(len) * p.nchunk;
+  for (uint64_t it = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
+    const uint32_t e = uint32_t(it / p.nchunk), c = uint32_t(it % p.nchunk);
+    const double tau = p.tau[e];
+    if (!(tau < __longlong_as_double(0x7ff0000000000000ll))) continue;
+    const float* y = p.tacs + uint64_t(p.list[e]) * p.L;
+    const uint64_t i0 = p.N * c / p.nchunk, i1 = p.N * (c + 1) / p.nchunk;
+    for (uint64_t i = i0 + lane; i < i1; i += 32) {
+      const float* s = p.bank + i * p.LS;
+      double D = 0.0;
+      bool rej = false;
+      for (uint32_t f = 0; f < p.L; ++f) {
+        const double d = __dsub_rn(double(__ldg(y + f)), double(__ldg(s + f)));
+        const double t = (p.dist == ABC_DIST_L1) ? fabs(d) : __dmul_rn(d, d);
+        D = __dadd_rn(D, __dmul_rn(double(__ldg(p.w + f)), t));
+        if (D > tau) { rej = true; break; }
+      }
+      if (!rej) {
+        const uint32_t pos = atomicAdd(p.cnt + e, 1u);
+        if (pos < p.cap) {
+          p.cd[uint64_t(e) * p.cap + pos] = D;
+          p.ci[uint64_t(e) * p.cap + pos] = uint32_t(i);
+        }
+      }
+    }
+  }
+}
+
+void launch_fallback_collect(const CollectParams& p, cudaStream_t st) {
+  fallback_collect_kernel<<<148 * 8, 256, 0, st>>>(p);
 }
 
 cudaError_t launch_certify_reduce(const ReduceParams& p, cudaStream_t st) {

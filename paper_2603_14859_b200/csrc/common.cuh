@@ -362,12 +362,47 @@ struct ReduceParams {
   // fallback output
   uint32_t* fb_list;
   uint32_t* fb_len;
-  int force_fb;       // ABC_FLAG_FORCE_FALLBACK: send every voxel to the exact scan (test hook)
+  int force_fb;       // ABC_FLAG_FORCE_FALLBACK: treat every voxel as uncertified (test hook)
   const int* bad;     // non-finite TACs: skip all work
+  // fallback tiers.  An uncertified voxel is appended to fb_list with fb_tau = the
+  // n-th smallest FP64 distance among its candidates (an upper bound on the exact tau64; +inf if
+  // unknown).  exact == 2: the candidates are the draws with D64 <= fb_tau collected for fb_list
+  // entry e by the fallback collector (cl_*); a voxel that cannot use them goes to fb2_list (exact
+  // heap scan, exact == 1).
+  double* fb_tau;            // [J] per fb_list entry
+  const double* cl_d;        // [cl_voxels][cl_cap]
+  const uint32_t* cl_i;      // [cl_voxels][cl_cap]
+  const uint32_t* cl_cnt;    // [cl_voxels]
+  uint32_t cl_cap, cl_voxels;
+  uint32_t* fb2_list;
+  uint32_t* fb2_len;
   // results (device pointers, may be null)
   abc_result out;
 };
 cudaError_t launch_certify_reduce(const ReduceParams& p, cudaStream_t st);
+// candidate capacity (a power of two >= 32) of the certification of p
+uint32_t certify_capacity(const ReduceParams& p);
+// Fallback collector: for fb_list entry e < min(*list_len, cap_voxels) with finite tau[e], every draw
+// with D64 <= tau[e] (FP64, operation for operation as the oracle; prefix pruning) is appended to
+// entry e's list (cnt[e] counts all of them, at most cap are stored).  The N draws of a voxel are
+// split into nchunk warp items spread over the whole GPU.
+struct CollectParams {
+  const float* bank;  // [N][LS]
+  uint64_t N;
+  uint32_t L, LS;
+  const float* tacs;
+  const float* w;
+  int dist;
+  const uint32_t* list;
+  const uint32_t* list_len;
+  const double* tau;
+  uint32_t cap_voxels, cap, nchunk;
+  uint32_t* cnt;
+  double* cd;
+  uint32_t* ci;
+  const int* bad;
+};
+void launch_fallback_collect(const CollectParams& p, cudaStream_t st);
 // Certification layouts: warp per voxel while the candidate set (a power of two) is <= kWarpCertifyMax,
 // else one CTA per voxel with up to kLargeMaxCand candidates in shared memory (196 KB).
 constexpr uint32_t kWarpCertifyMax = 2048;

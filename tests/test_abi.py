@@ -37,7 +37,7 @@ def test_struct_layouts():
     assert C.sizeof(_abi.Config) == 376
     assert _abi.Config.model.offset == 56
     assert C.sizeof(_abi.Result) == 11 * 8
-    assert C.sizeof(_abi.Stats) == 4 + 4 + 8 * 5 + 4 + 4 + 8 * 8
+    assert C.sizeof(_abi.Stats) == 4 + 4 + 8 * 6 + 4 + 4 + 8 * 8
 
 
 def test_init_rejects_bad_configs_before_touching_a_device():
