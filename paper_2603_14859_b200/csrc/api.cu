@@ -566,8 +566,10 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     // dense mode: a wider candidate band, since its dot-form error bound is ~1e-4 of ||y||^2 (vs ~u D)
     // FP32 pass: K = n + slack candidates per part.  The K-th smallest D32 is the pruning threshold, so
     // a small slack prunes harder; the slack (>= 1) only has to keep D_(K) above D_(n) + err for the
-    // certification, which 8 draws do with a wide margin at the paper's noise levels.
-    static const uint64_t slack = getenv("VPET_KSLACK") ? uint64_t(std::max(1, atoi(getenv("VPET_KSLACK")))) : 8;  // tuning knob
+    // certification: 4 draws left no uncertified voxel on the 4.44M-voxel TB volume
+    // (slack 2: 30 voxels; slack 1: 187 on the 1/32 slab set), and an uncertified voxel costs ~0.25 ms
+    // in the fallback collector.
+    static const uint64_t slack = getenv("VPET_KSLACK") ? uint64_t(std::max(1, atoi(getenv("VPET_KSLACK")))) : 4;  // tuning knob
     uint64_t k = dense ? 4 * uint64_t(n) + 64 : uint64_t(n) + std::max<uint64_t>(slack, n / 16);
     if (dense) k = (k + 7) & ~7ull;
     if (getenv("VPET_KROUND")) k = (k + 7) & ~7ull;  // tuning knob: round-1 behaviour
