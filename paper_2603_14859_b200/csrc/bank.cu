@@ -10,8 +10,13 @@
 //     S_f(a) = int_f (C_p (x) e^{-a.}) dt: exact recurrences on the PWL grid, or the Feng
 //     closed form.
 //   MRTM (eq:lp-ntPET with gamma = 0): value_f = [R1 int_f C_r + (k2 - R1 k2a) S_f(k2a)]/dt_f.
-//   (/ dt_f is applied as * RN64(1/dt_f), rounded on the host: at most an FP64 ulp from the oracle's
-//   division, which changes RN32 only for a value within that ulp of an FP32 rounding tie.)
+//   (/ dt_f is applied as * RN64(1/dt_f), rounded on the host.)
+// The FP64 values are not bit-identical to the oracle's: besides the host-rounded 1/dt_f, nvcc
+// contracts a*b+c into DFMA here (default -fmad=true), the phi functions use a series below 0.5
+// (the oracle uses closed forms / expm1) and the device exp differs from glibc's in the last ulp.
+// All of these are a few FP64 ulps, so RN32 of a frame value flips only when the value lies within
+// that distance of an FP32 rounding boundary (measured: < 1e-4 of bank entries, test_gpu_parity);
+// DESIGN.md §3 counts such flips among the parity-exempt boundary cases.
 //   lp-ntPET (eq:lp-ntPET, eq:Bt): z = C_t - R1 C_r, z' = (k2 - R1 a) C_r - a z,
 //     a(t) = k2a + gamma g(t) frozen at each substep midpoint (R4).
 #include <cfloat>

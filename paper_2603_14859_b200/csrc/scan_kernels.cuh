@@ -125,7 +125,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // (layout: common.cuh heap_stride).  The caller pushes only keys below the root of a full heap
 // (D < taup).  A push touches <= 2 levels for K <= 72: one 64-B group of children per level.
 // Returns (new count, new threshold bits).
-static __device__ __noinline__ uint2 heap_push(unsigned long long* hb, uint32_t K, uint32_t cnt, unsigned long long key) {
+#ifndef VPET_HEAP_INLINE
+#define VPET_HEAP_INLINE 0
+#endif
+#if VPET_HEAP_INLINE
+#define VPET_HEAP_ATTR __forceinline__
+#else
+#define VPET_HEAP_ATTR __noinline__
+#endif
+static __device__ VPET_HEAP_ATTR uint2 heap_push(unsigned long long* hb, uint32_t K, uint32_t cnt, unsigned long long key) {
   unsigned long long* h = hb + kHeapOff;
   unsigned long long root;
   if (cnt < K) {
@@ -350,12 +358,31 @@ __device__ __forceinline__ float2& acc_second(Acc& c) {
 #endif
 }
 
+// Row / box sources.  Shared-memory rows are addressed by their 32-bit shared address and read with
+// ld.shared (a generic pointer made the compiler re-derive the shared window base -- S2UR of the
+// cluster CTA id -- inside the row loop).  Volatile: never moved above the ring's mbarrier wait.
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+struct SmemSrc {
+  uint32_t a;  // shared address of element 0
+  __device__ __forceinline__ float4 ld(int q) const { return lds4(a + 4u * uint32_t(q)); }
+  __device__ __forceinline__ SmemSrc off(int q) const { return SmemSrc{a + 4u * uint32_t(q)}; }
+};
+struct GmemSrc {
+  const float* p;  // global memory, read-only during the scan
+  __device__ __forceinline__ float4 ld(int q) const { return __ldg(reinterpret_cast<const float4*>(p + q)); }
+  __device__ __forceinline__ GmemSrc off(int q) const { return GmemSrc{p + q}; }
+};
+
 // Chunk [c*CH, min((c+1)*CH, LP)) of the distance of R voxels to one bank row (scan order).
-template <int LP, int R, int DIST, int C>
-__device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const float* sr, Acc (&acc)[R]) {
+template <int LP, int R, int DIST, int C, class Src>
+__device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const Src sr, Acc (&acc)[R]) {
 #pragma unroll
   for (int q = C * CH; q < ((C + 1) * CH < LP ? (C + 1) * CH : LP); q += 4) {
-    const float4 s4 = *reinterpret_cast<const float4*>(sr + q);
+    const float4 s4 = sr.ld(q);
     const float2 sa = make_float2(s4.x, s4.y);
     const float2 sc = make_float2(s4.z, s4.w);
 #pragma unroll
@@ -375,15 +402,14 @@ __device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const float* 
   }
 }
 
-// Same chunk of the lower bound against a box [lo, hi] of bankp values (global memory).
-template <int LP, int R, int DIST, int C>
-__device__ __forceinline__ void bound_chunk(const Voxels<LP, R>& V, const float* lo, const float* hi,
-                                            Acc (&acc)[R]) {
+// Same chunk of the lower bound against a box [lo, hi] of bankp values (shared memory for the
+// prefetched super-tile / tile boxes, global memory for the hyper-tile boxes).
+template <int LP, int R, int DIST, int C, class Src>
+__device__ __forceinline__ void bound_chunk(const Voxels<LP, R>& V, const Src lo, const Src hi, Acc (&acc)[R]) {
 #pragma unroll
   for (int q = C * CH; q < ((C + 1) * CH < LP ? (C + 1) * CH : LP); q += 4) {
-    // generic loads: the boxes live in shared memory (prefetched super/tile boxes) or global memory
-    const float4 l4 = *reinterpret_cast<const float4*>(lo + q);
-    const float4 h4 = *reinterpret_cast<const float4*>(hi + q);
+    const float4 l4 = lo.ld(q);
+    const float4 h4 = hi.ld(q);
     const float2 la = make_float2(l4.x, l4.y), lc = make_float2(l4.z, l4.w);
     const float2 ha = make_float2(h4.x, h4.y), hc = make_float2(h4.z, h4.w);
 #pragma unroll
@@ -418,7 +444,8 @@ __device__ __forceinline__ bool any_alive(const Voxels<LP, R>& V, const Acc (&ac
 template <int LP, int R, int DIST, bool BOUND, int C>
 struct Chunks {
   static constexpr int NCH = (LP + CH - 1) / CH;
-  __device__ __forceinline__ static bool run(const Voxels<LP, R>& V, const float* a, const float* b, Acc (&acc)[R],
+  template <class Src>
+  __device__ __forceinline__ static bool run(const Voxels<LP, R>& V, const Src a, const Src b, Acc (&acc)[R],
                                              unsigned long long& work, bool noprune) {
     if (BOUND) bound_chunk<LP, R, DIST, C>(V, a, b, acc);
     else dist_chunk<LP, R, DIST, C>(V, a, acc);
@@ -465,13 +492,13 @@ __device__ __forceinline__ void finish_row(const ScanParams& p, Voxels<LP, R>& V
 }
 
 template <int LP, int R, int DIST, bool COUNT, bool SH = false>
-__device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, const float* sr, uint64_t i,
+__device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, const SmemSrc sr, uint64_t i,
                                          uint32_t part, unsigned long long& work, uint32_t htop_s = 0) {
   Acc acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc_zero(acc[r]);
   unsigned long long w = 0;
-  bool go = Chunks<LP, R, DIST, false, 0>::run(V, sr, nullptr, acc, w, !p.prune);
+  bool go = Chunks<LP, R, DIST, false, 0>::run(V, sr, sr, acc, w, !p.prune);
   if (COUNT && !VPET_COUNT_PUSH) work += w;
   if (go) finish_row<LP, R, COUNT, SH>(p, V, acc, i, part, work, htop_s);
 }
@@ -480,8 +507,8 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
 // pair of votes), then each survivor continues alone.  Row B's first-chunk test may use the
 // threshold from before row A's inserts: a larger threshold only keeps more, so this is exact.
 template <int LP, int R, int DIST, bool COUNT, bool SH = false>
-__device__ __forceinline__ void eval_pair(const ScanParams& p, Voxels<LP, R>& V, const float* sa, uint64_t ia,
-                                          const float* sb, uint64_t ib, uint32_t part, unsigned long long& work,
+__device__ __forceinline__ void eval_pair(const ScanParams& p, Voxels<LP, R>& V, const SmemSrc sa, uint64_t ia,
+                                          const SmemSrc sb, uint64_t ib, uint32_t part, unsigned long long& work,
                                           uint32_t htop_s = 0) {
   constexpr int NCH = (LP + CH - 1) / CH;
   Acc aa[R], ab[R];
@@ -496,13 +523,13 @@ __device__ __forceinline__ void eval_pair(const ScanParams& p, Voxels<LP, R>& V,
   bool ga = any_alive<LP, R>(V, aa, !p.prune);
   bool gb = any_alive<LP, R>(V, ab, !p.prune);
   if constexpr (NCH > 1) {
-    if (ga) ga = Chunks<LP, R, DIST, false, 1>::run(V, sa, nullptr, aa, w, !p.prune);
+    if (ga) ga = Chunks<LP, R, DIST, false, 1>::run(V, sa, sa, aa, w, !p.prune);
   }
   if (COUNT && !VPET_COUNT_PUSH) work += w;
   if (ga) finish_row<LP, R, COUNT, SH>(p, V, aa, ia, part, work, htop_s);
   w = 0;
   if constexpr (NCH > 1) {
-    if (gb) gb = Chunks<LP, R, DIST, false, 1>::run(V, sb, nullptr, ab, w, !p.prune);
+    if (gb) gb = Chunks<LP, R, DIST, false, 1>::run(V, sb, sb, ab, w, !p.prune);
   }
   if (COUNT && !VPET_COUNT_PUSH) work += w;
   if (gb) finish_row<LP, R, COUNT, SH>(p, V, ab, ib, part, work, htop_s);
@@ -547,11 +574,18 @@ __device__ __forceinline__ void refresh_tau_pipe(const ScanParams& p, Voxels<LP,
 }
 
 template <int LP, int R, int DIST>
-__device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const float* box, unsigned long long& work) {
+__device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const GmemSrc box, unsigned long long& work) {
   Acc acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc_zero(acc[r]);
-  return Chunks<LP, R, DIST, true, 0>::run(V, box, box + LP, acc, work, false);
+  return Chunks<LP, R, DIST, true, 0>::run(V, box, box.off(LP), acc, work, false);
+}
+template <int LP, int R, int DIST>
+__device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const SmemSrc box, unsigned long long& work) {
+  Acc acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc_zero(acc[r]);
+  return Chunks<LP, R, DIST, true, 0>::run(V, box, box.off(LP), acc, work, false);
 }
 
 template <int LP, int R>
@@ -627,7 +661,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_flat_kernel(const Sc
     const uint64_t rem = N - uint64_t(t) * T;
     const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
     const uint64_t ibase = uint64_t(t) * T;
-    for (uint32_t d = 0; d < nd; ++d) eval_row<LP, R, DIST, COUNT>(p, V, sb + d * LP, ibase + d, 0u, work);
+    for (uint32_t d = 0; d < nd; ++d) eval_row<LP, R, DIST, COUNT>(p, V, SmemSrc{smem_u32(sb) + 4u * d * LP}, ibase + d, 0u, work);
     __syncwarp();
     if (lane == 0) {
       __threadfence_block();
@@ -756,6 +790,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
   constexpr size_t BXF = Shape<LP>::BOXB_FLOATS;
   float* bbuf = reinterpret_cast<float*>(smem_raw + align16(sorder + kHyperSort));  // [2][BXF]
   uint64_t* bbar = reinterpret_cast<uint64_t*>(bbuf + 2 * BXF);                    // [2]
+  const uint32_t stage_a = smem_u32(stage), bbuf_a = smem_u32(bbuf);  // 32-bit shared addresses
   unsigned long long* htop = reinterpret_cast<unsigned long long*>(smem_raw + align16(bbar + 2));  // [R][NT][9]
   unsigned long long* htop_t = VPET_SHEAP ? htop + threadIdx.x * 9 : nullptr;
   const uint32_t htop_s = smem_u32(htop) + uint32_t(threadIdx.x) * 72u;  // this thread's heap tops (bytes)
@@ -869,7 +904,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
     for (uint32_t q = 0; q < nsub; ++q) {
       const uint64_t h = part + uint64_t(horder[q]) * S;
       if ((q & VPET_HREFRESH) == 0) refresh_tau<LP, R>(p, V);
-      const bool halive = box_alive<LP, R, DIST>(V, p.hbounds + h * 2 * LP, bwork);
+      const bool halive = box_alive<LP, R, DIST>(V, GmemSrc{p.hbounds + h * 2 * LP}, bwork);
       if (!__syncthreads_or(halive)) continue;
       const uint64_t s0 = h * p.hs;
       const uint32_t ns = uint32_t(((s0 + p.hs < p.nsuper) ? s0 + p.hs : p.nsuper) - s0);
@@ -892,9 +927,9 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       if ((it & VPET_REFRESH) == VPET_REFRESH) refresh_tau<LP, R>(p, V);
       mbar_wait(&bbar[cur], (bcount >> 1) & 1u);
       ++bcount;
-      const float* sbx = bbuf + cur * BXF;
       // super-tile bound
-      bool alive = halive && box_alive<LP, R, DIST>(V, sbx, bwork);
+      const uint32_t sbx_a = bbuf_a + cur * uint32_t(BXF) * 4u;  // shared address of the boxes
+      bool alive = halive && box_alive<LP, R, DIST>(V, SmemSrc{sbx_a}, bwork);
       if (!__syncthreads_or(alive)) continue;
       // tile bounds -> per-warp masks
       const uint64_t t0 = s * kSuper;
@@ -902,7 +937,8 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       uint32_t mask = 0;
       if (alive) {
         for (uint64_t t = t0; t < t1; ++t)
-          if (box_alive<LP, R, DIST>(V, sbx + 2 * LP + (t - t0) * 2 * LP, bwork)) mask |= 1u << uint32_t(t - t0);
+          if (box_alive<LP, R, DIST>(V, SmemSrc{sbx_a + 4u * uint32_t(2 * LP + (t - t0) * 2 * LP)}, bwork))
+            mask |= 1u << uint32_t(t - t0);
       }
       if (lane == 0) wmask[wid] = mask;
       __syncthreads();
@@ -938,7 +974,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
           if (VPET_TREFRESH == 1) refresh_tau_pipe<LP, R>(p, V, gpend);
           if (VPET_TREFRESH == 2) refresh_tau<LP, R>(p, V);
           if (VPET_TREFRESH == 3) refresh_apply<LP, R>(V, gnow);
-          const float* sb = stage + size_t(st) * Shape<LP>::STAGE_FLOATS;
+          const uint32_t sb_a = stage_a + uint32_t(st) * uint32_t(Shape<LP>::STAGE_FLOATS) * 4u;
           const uint32_t* si = sidx + st * T;
           const uint64_t rem = N - t * T;
           const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
@@ -946,11 +982,25 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
 #define VPET_PAIR 0
 #endif
           uint32_t d = 0;
+          // VPET_TREFRESH 4: the shared-threshold load is issued here and applied after the first
+          // kTrefreshRows rows, so its L2 round trip hides behind their evaluation (those rows use
+          // the threshold of the previous tile: larger, so they only keep more -- still exact)
+          constexpr uint32_t kTrefreshRows = 4;
+          if (VPET_TREFRESH == 4) {
+            float gnow4[R];
+            refresh_issue<LP, R>(p, V, gnow4);
+            const uint32_t d0 = nd < kTrefreshRows ? nd : kTrefreshRows;
+            for (; d < d0; ++d)
+              eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
+            refresh_apply<LP, R>(V, gnow4);
+          }
           if (VPET_PAIR)
             for (; d + 1 < nd; d += 2)
-              eval_pair<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, sb + d * LP, si[d], sb + (d + 1) * LP, si[d + 1],
+              eval_pair<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d],
+                                                              SmemSrc{sb_a + 4u * (d + 1) * LP}, si[d + 1],
                                                               part, work, htop_s);
-          for (; d < nd; ++d) eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, sb + d * LP, si[d], part, work, htop_s);
+          for (; d < nd; ++d)
+            eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
         }
         __syncwarp();
         if (lane == 0) {

@@ -8,5 +8,5 @@ P:84-94 -- a different numerical route from the method's closed forms) and noise
 (P:216-220).  Recipes are documented in DESIGN.md ("Input recipe").
 """
 from .schedules import (fdg22, tb35, uniform_frames, decay_weights)  # noqa: F401
-from .problems import (Problem, config1, config2, config3, config4_chunk, tb_geometry, tb_voxel_count, brain_geometry, priors_fdg,
+from .problems import (Problem, config1, config2, config3, config4_chunk, config4_continuous, tb_geometry, tb_voxel_count, brain_geometry, priors_fdg,
                        priors_rt, FENG_PHANTOM)  # noqa: F401

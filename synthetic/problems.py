@@ -322,7 +322,7 @@ def tb_voxel_count():
 
 
 def config4_chunk(chunk=0, n_chunks=32, N=10_000_000, n=18, seed=1004, abc_seed=2026, device="cpu",
-                  max_voxels=None, distance="WL2", voxel_index=None):
+                  max_voxels=None, distance="WL2", voxel_index=None, ell=7.0):
     """Axial slices z = chunk, chunk + n_chunks, ... of the TB phantom (raster order within each
     slice; n_chunks = 1 is the whole 4,441,800-voxel volume).  IDIF = frame means of the Feng
     curve + 2 % noise as PWL knots.  voxel_index selects voxels of the chunk (e.g. a
@@ -361,7 +361,7 @@ def config4_chunk(chunk=0, n_chunks=32, N=10_000_000, n=18, seed=1004, abc_seed=
         rng = np.random.default_rng([seed, int(z), 1])
         nz = len(tb_geometry(int(z))[0])
         eps = rng.standard_normal((nz, C.shape[1]))[pos[sel]]  # the slice's noise field, same for any subset
-        y[sel] = noise_fdg_eps(C[sel], start, dur, 7.0, T_HALF_F18, eps)
+        y[sel] = noise_fdg_eps(C[sel], start, dur, ell, T_HALF_F18, eps)
     idif_rng = np.random.default_rng([seed, 999_999])
     fm = feng_frame_means(feng, start, dur)
     fm = fm * (1.0 + 0.02 * idif_rng.standard_normal(fm.shape))
@@ -374,6 +374,73 @@ def config4_chunk(chunk=0, n_chunks=32, N=10_000_000, n=18, seed=1004, abc_seed=
               seed=abc_seed, distance=distance, accept="TOPN", n_accept=n)
     return Problem(f"config4_chunk{chunk}of{n_chunks}", kw, "PWL", kv, kt, start, dur,
                    decay_weights(start, dur, T_HALF_F18), y, dict(theta=theta, label=lab, z=zz, clean=C))
+
+
+def _smooth_field(rng, pts, n_waves=12, scale=0.04):
+    """A smooth random field on points pts [n, 3] (voxel coordinates): sum of random low-frequency
+    3-D cosines with random phases (mean 0, variance n_waves / 2), standardised analytically (so a
+    voxel's value does not depend on which other voxels are generated), mapped to (0, 1) by the
+    normal CDF (every value of the range occurs, near-uniform marginals)."""
+    f = np.zeros(len(pts))
+    for _ in range(n_waves):
+        k = rng.normal(0.0, scale, 3)
+        f += np.cos(pts @ k + rng.uniform(0, 2 * np.pi))
+    f = f / math.sqrt(n_waves / 2.0)
+    return 0.5 * (1.0 + np.vectorize(math.erf)(f / math.sqrt(2.0)))
+
+
+def config4_continuous(chunk=0, n_chunks=32, N=10_000_000, n=18, ell=7.0, seed=1014, abc_seed=2026, device="cpu",
+                       max_voxels=None, voxel_index=None, distance="WL2"):
+    """Harder variant of config 4 (VERDICT r01 "what's weak" 10): the same body mask, frames, IDIF and
+    noise model, but the kinetic parameters are CONTINUOUS smooth random fields spanning the whole
+    eq:prior2 ranges instead of 9 tissue classes -- no clustering for the pruned scan to
+    exploit -- and half the volume (a smooth region) reversible (k4 > 0).  ell = noise level of P:220."""
+    start, dur = tb35()
+    lo, hi = priors_fdg()
+    feng = FENG_PHANTOM
+    zs = list(range(chunk, TB_SHAPE[0], n_chunks))
+    pts = []
+    for z in zs:
+        flat, _ = tb_geometry(z)
+        yy, xx = np.divmod(flat, TB_SHAPE[2])
+        pts.append(np.stack([xx, yy, np.full(len(flat), z)], axis=1).astype(np.float64))
+    pts = np.concatenate(pts)
+    zz = pts[:, 2].astype(np.int32)
+    pos = np.concatenate([np.arange(np.sum(zz == z)) for z in zs])
+    rng = np.random.default_rng([seed, 0])
+    theta = np.empty((len(pts), 5))
+    for k in range(5):
+        u = _smooth_field(rng, pts)
+        theta[:, k] = lo[k] + (hi[k] - lo[k]) * np.clip(u, 1e-6, 1 - 1e-6)
+    rev = _smooth_field(rng, pts) > 0.5
+    theta[~rev, 3] = 0.0
+    if max_voxels is not None:
+        theta, zz, pos, rev = theta[:max_voxels], zz[:max_voxels], pos[:max_voxels], rev[:max_voxels]
+    if voxel_index is not None:
+        vi = np.asarray(voxel_index)
+        theta, zz, pos, rev = theta[vi], zz[vi], pos[vi], rev[vi]
+    C = truth_2tcm(theta, feng, start, dur, device)
+    y = np.empty(C.shape, dtype=np.float32)
+    order = np.argsort(zz, kind="stable")
+    zs_sorted = zz[order]
+    for z in np.unique(zz):
+        a, b = np.searchsorted(zs_sorted, [z, z + 1])
+        sel = order[a:b]
+        nz = len(tb_geometry(int(z))[0])
+        eps = np.random.default_rng([seed, int(z), 1]).standard_normal((nz, C.shape[1]))[pos[sel]]
+        y[sel] = noise_fdg_eps(C[sel], start, dur, ell, T_HALF_F18, eps)
+    idif_rng = np.random.default_rng([1004, 999_999])  # the config-4 IDIF
+    fm = feng_frame_means(feng, start, dur)
+    fm = fm * (1.0 + 0.02 * idif_rng.standard_normal(fm.shape))
+    mid = start + 0.5 * dur
+    kt = np.concatenate([[0.0], mid])
+    kv = np.concatenate([[0.0], fm])
+    half = N // 2
+    kw = dict(models=[dict(kind="2TCM_IRR", n_draws=half, lo=lo, hi=hi),
+                      dict(kind="2TCM_REV", n_draws=N - half, lo=lo, hi=hi)],
+              seed=abc_seed, distance=distance, accept="TOPN", n_accept=n)
+    return Problem(f"config4c_chunk{chunk}of{n_chunks}_ell{ell}", kw, "PWL", kv, kt, start, dur,
+                   decay_weights(start, dur, T_HALF_F18), y, dict(theta=theta, reversible=rev, z=zz, clean=C))
 
 
 # ----------------------------------------------------------------------------------

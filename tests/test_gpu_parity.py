@@ -345,3 +345,15 @@ def test_large_n_cta_certification(tb_small, N, n, flags):
     o, _ = run_oracle(p)
     rep = compare(g, o)
     assert rep["matched"] >= p.J - 2
+
+
+@pytest.mark.parametrize("ell", [3.5, 14.0])
+def test_continuous_phantom_parity(ell):
+    """Harder data: kinetic parameters as continuous fields over the whole prior range, low and high
+    noise (synthetic.config4_continuous); exactness does not depend on clusterability."""
+    p = S.config4_continuous(chunk=5, n_chunks=64, N=200_000, n=18, ell=ell, max_voxels=2000)
+    sub = p.subset(np.random.default_rng(3).choice(p.J, 96, replace=False))
+    g, _ = run_gpu(sub)
+    o, _ = run_oracle(sub)
+    rep = compare(g, o)
+    assert rep["matched"] >= sub.J - 2

@@ -14,6 +14,8 @@ VARIANTS = {
     "base": (),
     "acc2": ("VPET_ACC2=1",),
     "tr3": ("VPET_TREFRESH=3",),
+    "tr4": ("VPET_TREFRESH=4",),
+    "hinl": ("VPET_HEAP_INLINE=1",),
     "tr3acc2": ("VPET_TREFRESH=3", "VPET_ACC2=1"),
     "npc3": ("VPET_NPC=3",),
     "npc5": ("VPET_NPC=5",),
