@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "simulated draws/sec, voxels/sec and TB K_i-map time at 1/2/4/8 B200"
 TB_VOXELS = 4_441_800
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "scan_ncu_summary.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r02_scan_volume_ncu.json")
 
 
 def parse():
