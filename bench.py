@@ -307,7 +307,11 @@ def main():
             "executed_bound_updates_per_launch": bound_updates,
             "dense_equivalent_tflops": dense_equiv / 1e12,
             "pruned_fraction_of_dense": frame_updates / float(J * N * L),
-            "scan_ms": scan_s * 1e3, "scan_share_of_step": scan_s * 1e3 / statistics.median(step_ms)}
+            "scan_ms": scan_s * 1e3, "scan_share_of_step": scan_s * 1e3 / statistics.median(step_ms),
+            # the same executed lane-ops against the rate the FADD2+FFMA2 distance step itself reaches in
+            # the microbenchmark (115.7 lane-op/clk/SM, profiles/r02_fp_rates.txt)
+            "peak_measured_mix": 148 * 115.7 * sm_mhz * 1e6 / 1e12,
+            "frac_vs_measured_mix": achieved / (148 * 115.7 * sm_mhz * 1e6)}
     if os.path.exists(PROFILE_SUMMARY):
         try:
             ps = json.load(open(PROFILE_SUMMARY))
