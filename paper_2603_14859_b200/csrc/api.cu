@@ -949,6 +949,15 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   rp.fb_len = ctx->fb_len.as<uint32_t>();
   rp.force_fb = (ctx->cfg.flags & ABC_FLAG_FORCE_FALLBACK) ? 1 : 0;
   rp.bad = ctx->flag.as<int>();
+  // K3 / K4 split (warp layout only): the certification kernels write sorted accepted lists, one
+  // reduction kernel then summarises every voxel (smaller kernels: fewer instruction-cache misses)
+  static const bool split_env = getenv("VPET_SPLIT") ? atoi(getenv("VPET_SPLIT")) != 0 : true;  // tuning knob
+  const bool split = split_env && !eps && certify_capacity(rp) <= kWarpCertifyMax;
+  if (split) {
+    rp.list_only = 1;
+    rp.acc_i = ctx->hidx.as<uint32_t>();
+    rp.acc_d = ctx->hd.as<double>();
+  }
   if (cl_voxels) {
     rp.fb_tau = ctx->fb_tau.as<double>();
     rp.cl_d = ctx->cl_d.as<double>();
@@ -989,6 +998,10 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     rec(EV_CERT);
     CK(launch_certify_reduce(rp, st));
     launches += 2;
+    if (split) {
+      CK(launch_reduce_accepted_lists(rp, ctx->hidx.as<uint32_t>(), ctx->hd.as<double>(), ctx->flag.as<int>(), st));
+      ++launches;
+    }
     rec(EV_FB);
   } else {
     rp.exact = 0;
@@ -1042,6 +1055,10 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     rx.fb_list = nullptr;
     CK(launch_certify_reduce(rx, st));
     launches += 2;
+    if (split) {  // K4 for every voxel (certified or from a fallback tier)
+      CK(launch_reduce_accepted_lists(rp, ctx->hidx.as<uint32_t>(), ctx->hd.as<double>(), ctx->flag.as<int>(), st));
+      ++launches;
+    }
     rec(EV_FB);
   }
   CK(cudaGetLastError());

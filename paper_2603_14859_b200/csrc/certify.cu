@@ -11,6 +11,7 @@
 // ties -> model 0), conditional mean, SD (ddof 1) and type-7 quantiles of every column over
 // the accepted draws of the preferred model, and K_i = K1 k3/(k2+k3).
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -410,7 +411,14 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
         continue;
       }
     }
-    reduce_topn(p, v, ci, cd, sc, np2, lane);
+    if (p.list_only) {  // K3 only: the (D, i)-sorted accepted list; K4 runs once for all voxels
+      for (uint32_t a = lane; a < p.n; a += 32) {
+        p.acc_i[v * p.n + a] = ci[a];
+        p.acc_d[v * p.n + a] = cd[a];
+      }
+    } else {
+      reduce_topn(p, v, ci, cd, sc, np2, lane);
+    }
     __syncwarp();
   }
 }
@@ -813,14 +821,27 @@ __global__ void eps_reduce_kernel(const EpsReduceParams p) {
 // Warp per voxel: the first n_use indices of the voxel's list (e.g. a top-n list sorted by (D, i):
 // its prefix IS the top-n_use set of the same run, SURVEY §8f-3 "truncation of one max-n run")
 // are reduced exactly as K4 reduces a certified list.
-__global__ void reduce_list_kernel(const ReduceParams p, const uint64_t* idx, uint32_t n_acc, uint32_t np2, uint32_t wpc,
-                                   int* bad) {
+template <typename IdxT>
+__global__ void reduce_list_kernel(const ReduceParams p, const IdxT* idx, const double* dist, uint32_t n_acc, uint32_t np2,
+                                   uint32_t wpc, int* bad) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const uint32_t w = threadIdx.x >> 5;
   const size_t per_warp = size_t(np2) * 12;
   double* sc = reinterpret_cast<double*>(smem_raw + per_warp * w);
   uint32_t* ci = reinterpret_cast<uint32_t*>(sc + np2);
+  if (p.bad && *p.bad) return;
+  for (uint64_t v = uint64_t(blockIdx.x) * wpc + w; v < p.J; v += uint64_t(gridDim.x) * wpc) {
+      const bool in = uint32_t(lane) < p.n;
+      uint64_t i = in ? uint64_t(idx[v * n_acc + lane]) : 0;
+      if (i >= p.N) {
+        atomicExch(bad, 1);
+        i = 0;
+      }
+      reduce_small(p, v, uint32_t(i), (in && dist) ? dist[v * n_acc + lane] : 0.0, dist != nullptr, lane);
+    }
+    return;
+  }
   for (uint64_t v = uint64_t(blockIdx.x) * wpc + w; v < p.J; v += uint64_t(gridDim.x) * wpc) {
     for (uint32_t a = lane; a < p.n; a += 32) {
       const uint64_t i = idx[v * n_acc + a];
@@ -828,7 +849,7 @@ __global__ void reduce_list_kernel(const ReduceParams p, const uint64_t* idx, ui
       ci[a] = uint32_t(i < p.N ? i : 0);
     }
     __syncwarp();
-    reduce_topn(p, v, ci, nullptr, sc, np2, lane);
+    reduce_topn(p, v, ci, dist ? dist + v * n_acc : nullptr, sc, np2, lane);
     __syncwarp();
   }
 }
@@ -1014,20 +1035,31 @@ void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st) {
   eps_reduce_kernel<<<unsigned(blocks), 128, 0, st>>>(p);
 }
 
-cudaError_t launch_reduce_list(const ReduceParams& p, const uint64_t* idx, uint32_t n_acc, int* bad, cudaStream_t st) {
+template <typename IdxT>
+static cudaError_t launch_reduce_list_t(const ReduceParams& p, const IdxT* idx, const double* dist, uint32_t n_acc,
+                                        int* bad, cudaStream_t st) {
   uint32_t np2 = next_pow2(p.n);
   if (np2 < 32) np2 = 32;
   const size_t per_warp = size_t(np2) * 12;
   uint32_t wpc = 8;
   while (wpc > 1 && per_warp * wpc > 96 * 1024) wpc >>= 1;
   const size_t smem = per_warp * wpc;
-  cudaError_t e = ensure_smem_attr((const void*)reduce_list_kernel, smem);
+  cudaError_t e = ensure_smem_attr((const void*)reduce_list_kernel<IdxT>, smem);
   if (e != cudaSuccess) return e;
   uint64_t blocks = (p.J + wpc - 1) / wpc;
   if (blocks > 148ull * 32) blocks = 148ull * 32;
   if (blocks == 0) blocks = 1;
-  reduce_list_kernel<<<unsigned(blocks), wpc * 32, smem, st>>>(p, idx, n_acc, np2, wpc, bad);
+  reduce_list_kernel<IdxT><<<unsigned(blocks), wpc * 32, smem, st>>>(p, idx, dist, n_acc, np2, wpc, bad);
   return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_list(const ReduceParams& p, const uint64_t* idx, uint32_t n_acc, int* bad, cudaStream_t st) {
+  return launch_reduce_list_t<uint64_t>(p, idx, nullptr, n_acc, bad, st);
+}
+
+cudaError_t launch_reduce_accepted_lists(const ReduceParams& p, const uint32_t* idx, const double* dist, int* bad,
+                                         cudaStream_t st) {
+  return launch_reduce_list_t<uint32_t>(p, idx, dist, p.n, bad, st);
 }
 
 cudaError_t launch_response_envelope(const EnvelopeParams& p, cudaStream_t st) {

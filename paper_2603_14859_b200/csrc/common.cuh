@@ -376,6 +376,11 @@ struct ReduceParams {
   uint32_t cl_cap, cl_voxels;
   uint32_t* fb2_list;
   uint32_t* fb2_len;
+  // list_only: the certification (warp layout) writes each voxel's (D, i)-sorted accepted list to
+  // acc_i / acc_d ([J][n]) instead of reducing it; launch_reduce_accepted_lists reduces them all
+  int list_only;
+  uint32_t* acc_i;
+  double* acc_d;
   // results (device pointers, may be null)
   abc_result out;
 };
@@ -410,6 +415,9 @@ constexpr uint32_t kLargeMaxCand = 16384;
 constexpr uint32_t kMaxAccept = 15360;  // n_accept cap: n + n/16 slack <= kLargeMaxCand (one part)
 // K4 on given accepted lists (abc_reduce_accepted): the first p.n of n_acc indices per voxel.
 cudaError_t launch_reduce_list(const ReduceParams& p, const uint64_t* idx, uint32_t n_acc, int* bad, cudaStream_t st);
+// K4 over the accepted lists written by list_only certification (u32 indices, FP64 distances).
+cudaError_t launch_reduce_accepted_lists(const ReduceParams& p, const uint32_t* idx, const double* dist, int* bad,
+                                         cudaStream_t st);
 
 // Response-function envelope (Fig. 1): abc_response_envelope.
 struct EnvelopeParams {

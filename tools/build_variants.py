@@ -16,6 +16,10 @@ VARIANTS = {
     "tr3": ("VPET_TREFRESH=3",),
     "tr4": ("VPET_TREFRESH=4",),
     "hinl": ("VPET_HEAP_INLINE=1",),
+    "pair": ("VPET_PAIR=1",),
+    "nst3": ("VPET_NST=3",),
+    "ch12": ("VPET_CH=12",),
+    "ch20": ("VPET_CH=20",),
     "tr3acc2": ("VPET_TREFRESH=3", "VPET_ACC2=1"),
     "npc3": ("VPET_NPC=3",),
     "npc5": ("VPET_NPC=5",),

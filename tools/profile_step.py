@@ -46,6 +46,7 @@ for s in range(a.steps):
     r = ctx.run_voxels(y, want=("prob", "preferred", "count", "mean", "sd", "q", "ki_mean", "ki_sd", "ki_q"))
     st = ctx.stats()
     print(f"step {s}: {time.time() - t:.3f} s  scan {st['ms_scan']:.1f} ms  order {st['ms_order']:.1f} ms  "
-          f"bank {st['ms_bank']:.1f} ms  certify {st['ms_certify']:.2f} ms  fallback voxels {st['n_fallback']}  "
+          f"bank {st['ms_bank']:.1f} ms  certify {st['ms_certify']:.2f} ms  fb+reduce {st['ms_fallback']:.2f} ms  "
+          f"total {st['ms_total']:.2f} ms  fallback voxels {st['n_fallback']}  "
           f"launches {st['gpu_launches']}" + (f"  frame_updates {st['frame_updates']}  bound_updates {st['bound_updates']}"
                                               if a.flags & 4 else ""), flush=True)
