@@ -832,17 +832,6 @@ __global__ void reduce_list_kernel(const ReduceParams p, const IdxT* idx, const 
   uint32_t* ci = reinterpret_cast<uint32_t*>(sc + np2);
   if (p.bad && *p.bad) return;
   for (uint64_t v = uint64_t(blockIdx.x) * wpc + w; v < p.J; v += uint64_t(gridDim.x) * wpc) {
-      const bool in = uint32_t(lane) < p.n;
-      uint64_t i = in ? uint64_t(idx[v * n_acc + lane]) : 0;
-      if (i >= p.N) {
-        atomicExch(bad, 1);
-        i = 0;
-      }
-      reduce_small(p, v, uint32_t(i), (in && dist) ? dist[v * n_acc + lane] : 0.0, dist != nullptr, lane);
-    }
-    return;
-  }
-  for (uint64_t v = uint64_t(blockIdx.x) * wpc + w; v < p.J; v += uint64_t(gridDim.x) * wpc) {
     for (uint32_t a = lane; a < p.n; a += 32) {
       const uint64_t i = idx[v * n_acc + a];
       if (i >= p.N) atomicExch(bad, 1);
