@@ -99,3 +99,23 @@ def test_brain_slices_stratified_oracle_parity(brain_slices):
     # the activated striatum is the lp-ntPET class (qualitative)
     act = p.truth["label"] == 5
     assert np.mean(g["prob"][act, 1] > 0.5) > 0.8
+
+
+def test_continuous_phantom_fullN_oracle_parity():
+    """Harder data at the full draw budget: the continuous-parameter TB phantom at double noise
+    (ell = 14), the 283,800 voxels of the slab set z = 0 mod 16 run through the GPU path at
+    N = 1e7 (every tree level active, the slowest case of profiles/r02_hard_phantoms.json), and the
+    oracle re-runs 64 of them."""
+    import torch
+    from paper_2603_14859_b200 import AbcContext
+    p = S.config4_continuous(chunk=0, n_chunks=16, N=10_000_000, n=18, ell=14.0, device="cuda")
+    ctx = AbcContext(**p.ctx_kwargs)
+    p.setup(ctx)
+    g = {k: v.cpu().numpy() for k, v in ctx.run_voxels(torch.from_numpy(p.tacs).cuda()).items()}
+    g["count"] = g["count"].view(np.uint32)
+    g["acc_idx"] = g["acc_idx"].view(np.uint64)
+    del ctx
+    idx = np.sort(np.random.default_rng(11).choice(p.J, 64, replace=False))
+    o = _oracle(p, p.tacs[idx])
+    rep = compare({k: v[idx] for k, v in g.items()}, o)
+    assert rep["matched"] >= len(idx) - 2, rep
