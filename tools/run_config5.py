@@ -16,7 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 import synthetic as S  # noqa: E402
-from paper_2603_14859_b200 import FLAG_DENSE_TC, FLAG_TIMING, AbcContext  # noqa: E402
+from paper_2603_14859_b200 import FLAG_DENSE_TC, FLAG_TIMING, AbcContext, AbcError  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--J", type=int, default=1 << 17)
@@ -24,6 +24,7 @@ ap.add_argument("--draws", default="10000,100000,1000000")
 ap.add_argument("--p", default="0.001,0.01")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--modes", default="fp32,dense")
+ap.add_argument("--out", default=None)
 a = ap.parse_args()
 
 base = S.config4_chunk(chunk=0, n_chunks=32, N=10_000, n=18, max_voxels=a.J, device="cuda")
@@ -41,9 +42,16 @@ for N in [int(x) for x in a.draws.split(",")]:
             ctx = AbcContext(**dict(prob.ctx_kwargs, flags=flags))
             prob.setup(ctx)
             sts, res = [], None
-            for _ in range(max(1, a.reps) + 1):
-                res = ctx.run_voxels(prob.tacs, want=("acc_idx", "prob"))
-                sts.append(ctx.stats())
+            try:
+                for _ in range(max(1, a.reps) + 1):
+                    res = ctx.run_voxels(prob.tacs, want=("acc_idx", "prob"))
+                    sts.append(ctx.stats())
+            except AbcError as e:  # e.g. the dense mode's candidate band exceeds its capacity at large n
+                row = {"N": N, "p": p, "n": n, "J": prob.J, "mode": mode, "unsupported": str(e)}
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+                ctx.close()
+                continue
             sts = sts[1:]
             med = {k: float(np.median([s[k] for s in sts])) for k in ("ms_total", "ms_bank", "ms_order", "ms_scan",
                                                                       "ms_certify", "ms_fallback")}
@@ -60,3 +68,5 @@ for N in [int(x) for x in a.draws.split(",")]:
             print(json.dumps(row), flush=True)
             ctx.close()
 print(json.dumps({"config5": rows}))
+if a.out:
+    open(a.out, "w").write(json.dumps({"config5": rows}, indent=1))
