@@ -953,6 +953,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   // reduction kernel then summarises every voxel (smaller kernels: fewer instruction-cache misses)
   static const bool split_env = getenv("VPET_SPLIT") ? atoi(getenv("VPET_SPLIT")) != 0 : true;  // tuning knob
   const bool split = split_env && !eps && certify_capacity(rp) <= kWarpCertifyMax;
+  static const bool reg_sort_env = getenv("VPET_REG_SORT") ? atoi(getenv("VPET_REG_SORT")) != 0 : true;  // tuning knob
+  rp.reg_sort = reg_sort_env ? 1 : 0;
   if (split) {
     rp.list_only = 1;
     rp.acc_i = ctx->hidx.as<uint32_t>();

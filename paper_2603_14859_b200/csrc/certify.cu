@@ -187,6 +187,21 @@ __device__ __forceinline__ bool column_exists(int kind, uint32_t k) {
   return k < ((kind >= ABC_MRTM) ? 7u : 5u);
 }
 
+// Ascending bitonic sort of one value per lane across the warp; returns this lane's sorted value.
+template <typename T>
+__device__ __forceinline__ T warp_sort32(T x, int lane) {
+#pragma unroll
+  for (uint32_t size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      const T o = __shfl_xor_sync(0xffffffffu, x, stride);
+      const bool lower = (uint32_t(lane) & stride) == 0, asc = (uint32_t(lane) & size) == 0;
+      if ((lower == asc) ? (x > o) : (o > x)) x = o;
+    }
+  }
+  return x;
+}
+
 // Reduce the sorted accepted list (ci[0..n)) of voxel v.  sc: np2 doubles of scratch.
 __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* ci, const double* cd, double* sc,
                             uint32_t np2, int lane) {
@@ -244,6 +259,33 @@ __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* c
     if (exists) {
       uint32_t npos = 0;
       double sum = 0.0;
+      if (small && p.reg_sort) {
+        // n <= 32, one value per lane: sums by warp_sum (same order as below), the order statistics
+        // by a register bitonic sort across the lanes -- FP32 for the parameter columns (the
+        // values ARE FP32; half the shuffles of FP64), FP64 for K_i; +inf pads the other lanes
+        const double x = !mine0 ? 0.0
+                         : (is_ki ? double(thr[0]) * double(thr[2]) / (double(thr[1]) + double(thr[2])) : double(thr[k]));
+        const double mu = warp_sum(x) / double(c);
+        const double ss = warp_sum(mine0 ? (x - mu) * (x - mu) : 0.0);
+        double xs;
+        if (is_ki) {
+          xs = warp_sort32<double>(mine0 ? x : __longlong_as_double(0x7ff0000000000000ll), lane);
+        } else {
+          xs = double(warp_sort32<float>(mine0 ? thr[k] : __int_as_float(0x7f800000), lane));
+        }
+        mean = float(mu);
+        sd = c >= 2 ? float(sqrt(ss / double(c - 1))) : NANF;
+        const double qs[3] = {0.025, 0.5, 0.975};
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const double h = double(c - 1) * qs[t];
+          const uint32_t lo = uint32_t(floor(h));
+          const uint32_t hi = lo + 1 < c ? lo + 1 : lo;
+          const double xl = __shfl_sync(0xffffffffu, xs, int(lo));
+          const double xh = __shfl_sync(0xffffffffu, xs, int(hi));
+          q3[t] = float(lo + 1 < c ? xl + (h - double(lo)) * (xh - xl) : xl);
+        }
+      } else {
       if (small) {
         if (mine0) {
           double x = is_ki ? double(thr[0]) * double(thr[2]) / (double(thr[1]) + double(thr[2])) : double(thr[k]);
@@ -283,6 +325,7 @@ __device__ void reduce_topn(const ReduceParams& p, uint64_t v, const uint32_t* c
       q3[1] = float(quantile7(sc, c, 0.5));
       q3[2] = float(quantile7(sc, c, 0.975));
       __syncwarp();
+      }
     }
     if (lane == 0) {
       if (is_ki) {

@@ -381,6 +381,7 @@ struct ReduceParams {
   int list_only;
   uint32_t* acc_i;
   double* acc_d;
+  int reg_sort;  // n <= 32: order statistics by register sorts across the lanes (K4)
   // results (device pointers, may be null)
   abc_result out;
 };
