@@ -703,7 +703,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(ctx->fb2_list.ensure(4 * J));
     CK(ctx->fb2_len.ensure(16));
   }
-  CK(ctx->work.ensure(16));
+  CK(ctx->work.ensure(32));
   CK(ctx->flag.ensure(16));
   if (host_tacs) CK(ctx->tacs.ensure(sizeof(float) * J * L));
   if (out_bytes) CK(ctx->outs.ensure(out_bytes));
@@ -758,7 +758,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(cudaMemsetAsync(ctx->fb2_len.p, 0, 16, st));
     CK(cudaMemsetAsync(ctx->cl_cnt.p, 0, size_t(4) * cl_voxels, st));
   }
-  CK(cudaMemsetAsync(ctx->work.p, 0, 16, st));
+  CK(cudaMemsetAsync(ctx->work.p, 0, 32, st));
   bool joined = false;
   auto join_tacs = [&]() -> cudaError_t {  // before the first kernel that reads the TACs
     if (joined) return cudaSuccess;
@@ -1085,6 +1085,11 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   S.gpu_launches = launches;
   S.n_fallback = h_fb;
   S.n_fallback_exact = cl_voxels ? h_fb2 : h_fb;
+  if (getenv("VPET_UNION_STATS") || getenv("VPET_PUSH_STATS")) {  // diagnostic counters of a VPET_UNION_STATS build (scan_kernels.cuh)
+    unsigned long long u[2] = {0, 0};
+    CK(cudaMemcpy(u, static_cast<unsigned long long*>(ctx->work.p) + 2, 16, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "diag counters: work[2] %llu, work[3] %llu (union stats: evaluated / alive voxel-lane tiles; push stats: pushes in work[3])\n", u[0], u[1]);
+  }
   S.frame_updates = h_work[0];
   S.bound_updates = h_work[1];
   if (timing) {

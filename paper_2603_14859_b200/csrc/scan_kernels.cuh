@@ -479,6 +479,9 @@ __device__ __forceinline__ void finish_row(const ScanParams& p, Voxels<LP, R>& V
         unsigned long long* hb = p.heap + (uint64_t(V.vox[r]) * p.nparts + part) * heap_stride(p.K);
         uint2 st = SH ? heap_push_s(hb, htop_s + uint32_t(r) * NT * 72u, p.K, V.cnt[r], key)
                       : heap_push(hb, p.K, V.cnt[r], key);
+#ifdef VPET_PUSH_STATS
+        atomicAdd(p.work + 3, 1ull);
+#endif
         V.cnt[r] = st.x;
         V.taup[r] = __uint_as_float(st.y);
         if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + V.vox[r], st.y);
@@ -680,11 +683,12 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_flat_kernel(const Sc
   finish_counts(p, work, 0ull, lane, COUNT);
 }
 
-// Ascending bitonic sort of P2 (a power of two) keys in shared memory by the whole CTA.
+// Ascending bitonic sort of P2 (a power of two) keys in shared memory by the whole CTA (NTH threads).
+template <int NTH>
 __device__ __forceinline__ void cta_bitonic(unsigned long long* key, uint32_t P2, int tid) {
   for (uint32_t kk = 2; kk <= P2; kk <<= 1) {
     for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
-      for (uint32_t i = tid; i < P2; i += NT) {
+      for (uint32_t i = tid; i < P2; i += NTH) {
         const uint32_t l = i ^ jj;
         if (l > i) {
           const unsigned long long a = key[i], b = key[l];
@@ -700,18 +704,20 @@ __device__ __forceinline__ void cta_bitonic(unsigned long long* key, uint32_t P2
 // its mean TAC (lbs[w][k]); the CTA order alternates between the warps' rankings (warp 0's best,
 // warp 1's best, warp 0's second, ...) skipping boxes already taken and warps without voxels.
 // keys: [NW * kHyperSort] scratch; order: [kHyperSort] output; vis: [kHyperSort / 32] scratch.
-__device__ __forceinline__ void best_first(const float* lbs, uint32_t n, unsigned long long* keys, uint32_t* order,
-                                           uint32_t* vis, int tid) {
+template <int NTH>
+__device__ __forceinline__ void best_first_n(const float* lbs, uint32_t n, unsigned long long* keys, uint32_t* order,
+                                             uint32_t* vis, int tid) {
+  constexpr int NW = NTH / 32;
   uint32_t P2 = 1;
   while (P2 < n) P2 <<= 1;
-  for (uint32_t e = tid; e < NW * P2; e += NT) {
+  for (uint32_t e = tid; e < NW * P2; e += NTH) {
     const uint32_t w = e / P2, k = e % P2;
     const uint32_t lbb = k < n ? __float_as_uint(lbs[w * kHyperSort + k]) : 0x7fffffffu;
     keys[e] = (static_cast<unsigned long long>(w) << 62) | (static_cast<unsigned long long>(lbb) << 16) | k;
   }
-  for (uint32_t e = tid; e < kHyperSort / 32; e += NT) vis[e] = 0u;
+  for (uint32_t e = tid; e < kHyperSort / 32; e += NTH) vis[e] = 0u;
   __syncthreads();
-  cta_bitonic(keys, NW * P2, tid);
+  cta_bitonic<NTH>(keys, NW * P2, tid);
   if (tid == 0) {
     uint32_t ptr[NW];
 #pragma unroll
@@ -895,7 +901,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       }
     }
     __syncthreads();
-    best_first(hlb, uint32_t(nsub), okeys, horder, vis, tid);
+    best_first_n<NT>(hlb, uint32_t(nsub), okeys, horder, vis, tid);
 
     uint32_t it = 0;
     float gpend[R];
@@ -914,7 +920,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
           hlb[wid * kHyperSort + k] =
               wvalid ? mean_lb<LP>(ybar + wid * LP, p.sbounds + (s0 + k) * 2 * LP) : __int_as_float(0x7f800000);
         __syncthreads();
-        best_first(hlb, ns, okeys, sorder, vis, tid);
+        best_first_n<NT>(hlb, ns, okeys, sorder, vis, tid);
       }
       for (uint32_t u = 0; u < ns; ++u, ++it) {
       const uint64_t s = s0 + (ssort ? sorder[u] : u);
@@ -940,6 +946,32 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
           if (box_alive<LP, R, DIST>(V, SmemSrc{sbx_a + 4u * uint32_t(2 * LP + (t - t0) * 2 * LP)}, bwork))
             mask |= 1u << uint32_t(t - t0);
       }
+#ifdef VPET_UNION_STATS
+      // diagnostic: voxel-lanes a warp evaluates per tile (R x 32) vs those whose own complete tile
+      // bound is below their threshold (the work a per-(tile, voxel) schedule would do)
+      if (COUNT && alive) {
+        unsigned long long ev = 0, al = 0;
+        for (uint32_t b = 0; b < uint32_t(t1 - t0); ++b) {
+          if (!((mask >> b) & 1u)) continue;
+          Acc acc[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc_zero(acc[r]);
+          unsigned long long dummy = 0;
+          const SmemSrc bx{sbx_a + 4u * uint32_t(2 * LP + b * 2 * LP)};
+          Chunks<LP, R, DIST, true, 0>::run(V, bx, bx.off(LP), acc, dummy, true);
+          int c = 0;
+#pragma unroll
+          for (int r = 0; r < R; ++r) c += (acc_total(acc[r]) < V.tau[r]) ? 1 : 0;
+          c = __reduce_add_sync(0xffffffffu, c);
+          ev += uint64_t(R) * 32u;
+          al += uint64_t(c);
+        }
+        if (lane == 0) {
+          atomicAdd(p.work + 2, ev);
+          atomicAdd(p.work + 3, al);
+        }
+      }
+#endif
       if (lane == 0) wmask[wid] = mask;
       __syncthreads();
       uint32_t cm = 0;

@@ -17,6 +17,8 @@ VARIANTS = {
     "tr4": ("VPET_TREFRESH=4",),
     "hinl": ("VPET_HEAP_INLINE=1",),
     "pair": ("VPET_PAIR=1",),
+    "union": ("VPET_UNION_STATS=1",),
+    "pushstats": ("VPET_PUSH_STATS=1",),
     "minb9": ("VPET_MINB=9",),
     "minb10": ("VPET_MINB=10",),
     "nst3": ("VPET_NST=3",),
