@@ -269,6 +269,51 @@ __device__ __forceinline__ unsigned long long spread_npc(unsigned long long x) {
 #ifndef VPET_BANK_MSB
 #define VPET_BANK_MSB 0
 #endif
+// Space-filling curve of the draw order: VPET_HILBERT = 1 Hilbert (12 % fewer executed frame updates
+// than Morton on the TB slab set, scan -2 %), 0 Morton (Z-order).
+// A Hilbert curve has no long jumps at cell boundaries, so a run of consecutive keys (a tile of 32
+// draws, a warp of 64 voxels) covers a more compact region: tighter tile boxes, more similar
+// voxels per warp (the order is free for exactness).
+#ifndef VPET_HILBERT
+#define VPET_HILBERT 1
+#endif
+#ifndef VPET_HILBERT_VOX
+#define VPET_HILBERT_VOX 0  // the voxel order stays Morton: the scan's queue takes voxel tiles from both
+                            // ends of the PC1-major Morton range first (the long items); a Hilbert voxel
+                            // order cut 3 % more work but lost that longest-first schedule (+30 % scan)
+#endif
+// Skilling's transpose form of the n-dimensional Hilbert index (J. Skilling, "Programming the
+// Hilbert curve", AIP Conf. Proc. 707, 2004): coordinates X[n] of b bits -> the transposed index,
+// bit-interleaved with X[0] the most significant bit of each group of n.
+template <int n, int b>
+__device__ __forceinline__ unsigned long long hilbert_key(uint32_t (&X)[n]) {
+  const uint32_t M = 1u << (b - 1);
+  for (uint32_t Q = M; Q > 1; Q >>= 1) {  // inverse undo
+    const uint32_t P = Q - 1;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      if (X[i] & Q) {
+        X[0] ^= P;
+      } else {
+        const uint32_t t = (X[0] ^ X[i]) & P;
+        X[0] ^= t;
+        X[i] ^= t;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 1; i < n; ++i) X[i] ^= X[i - 1];  // Gray encode
+  uint32_t t = 0;
+  for (uint32_t Q = M; Q > 1; Q >>= 1)
+    if (X[n - 1] & Q) t ^= Q - 1;
+#pragma unroll
+  for (int i = 0; i < n; ++i) X[i] ^= t;
+  unsigned long long key = 0;
+  for (int bit = b - 1; bit >= 0; --bit)
+#pragma unroll
+    for (int i = 0; i < n; ++i) key = (key << 1) | ((X[i] >> bit) & 1u);
+  return key;
+}
 __device__ __forceinline__ unsigned long long spread4(unsigned long long x) {
   // insert 3 zero bits between the low 16 bits of x (4-D Morton)
   unsigned long long r = 0;
@@ -299,12 +344,15 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
       for (int c = 0; c < kNPC; ++c) pr[c] = p.proj[i * kNPC + c];
     }
     unsigned long long key = 0;
+    uint32_t X[kNPC];
 #pragma unroll
     for (int c = 0; c < kNPC; ++c) {
       const float sc = c == 0 ? sm_scale : sm_scale * VPET_BANKS;
       float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sc, 0.0f), float((1u << kMBits) - 1u));
-      key |= spread_npc((unsigned long long)q) << (VPET_BANK_MSB ? kNPC - 1 - c : c);
+      X[c] = uint32_t(q);
+      if (!VPET_HILBERT) key |= spread_npc((unsigned long long)q) << (VPET_BANK_MSB ? kNPC - 1 - c : c);
     }
+    if (VPET_HILBERT) key = hilbert_key<kNPC, kMBits>(X);
     p.keys[i] = key;
     p.vals[i] = uint32_t(i);
   }
@@ -480,12 +528,15 @@ __global__ void __launch_bounds__(256) voxel_key_kernel(const VoxelOrderParams p
       key = f2ord(pr[0]);
     } else {
       const float top = float((1u << kVoxAxisBits) - 1u);
+      uint32_t X[kVoxDims];
 #pragma unroll
       for (int c = 0; c < kVoxDims; ++c) {
         const float sc = c == 0 ? sm_scale : (c == 1 ? sm_scale * VPET_VOXS : sm_scale * VPET_VOXS3);
         const float q = fminf(fmaxf((pr[c] - sm_lo[c]) * sc, 0.0f), top);
-        key |= spread_d((unsigned long long)q) << (kVoxDims - 1 - c);
+        X[c] = uint32_t(q);
+        if (!VPET_HILBERT_VOX) key |= spread_d((unsigned long long)q) << (kVoxDims - 1 - c);
       }
+      if (VPET_HILBERT_VOX) key = hilbert_key<kVoxDims, kVoxAxisBits>(X);
     }
     p.keys[j] = key;
     p.vals[j] = uint32_t(j);

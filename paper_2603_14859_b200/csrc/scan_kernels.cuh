@@ -290,7 +290,13 @@ __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& 
   const float INF = __int_as_float(0x7f800000);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    uint64_t slot = vtile * (NT * R) + uint64_t(r) * NT + tid;
+#ifndef VPET_WARP_CONTIG
+#define VPET_WARP_CONTIG 1
+#endif
+    // a warp's 32 R voxels are one contiguous run of the voxel order (the most similar TACs: a tile
+    // is evaluated for all of them once its bound is alive for one)
+    const uint64_t slot = VPET_WARP_CONTIG ? vtile * (NT * R) + uint64_t(tid >> 5) * (32 * R) + uint64_t(r) * 32 + (tid & 31)
+                                           : vtile * (NT * R) + uint64_t(r) * NT + tid;
     bool valid = slot < p.J;
     uint64_t v = (valid && p.vorder) ? uint64_t(__ldg(p.vorder + slot)) : slot;
     V.vox[r] = uint32_t(v);

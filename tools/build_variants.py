@@ -19,6 +19,11 @@ VARIANTS = {
     "pair": ("VPET_PAIR=1",),
     "union": ("VPET_UNION_STATS=1",),
     "pushstats": ("VPET_PUSH_STATS=1",),
+    "nocontig": ("VPET_WARP_CONTIG=0",),
+    "morton": ("VPET_HILBERT=0",),
+    "hbank": ("VPET_HILBERT=1", "VPET_HILBERT_VOX=0"),
+    "hvox": ("VPET_HILBERT=0", "VPET_HILBERT_VOX=1"),
+    "union_contig": ("VPET_UNION_STATS=1",),
     "minb9": ("VPET_MINB=9",),
     "minb10": ("VPET_MINB=10",),
     "nst3": ("VPET_NST=3",),
