@@ -1085,10 +1085,13 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   S.gpu_launches = launches;
   S.n_fallback = h_fb;
   S.n_fallback_exact = cl_voxels ? h_fb2 : h_fb;
-  if (getenv("VPET_UNION_STATS") || getenv("VPET_PUSH_STATS")) {  // diagnostic counters of a VPET_UNION_STATS build (scan_kernels.cuh)
+  if (getenv("VPET_UNION_STATS") || getenv("VPET_PUSH_STATS") || getenv("VPET_TRAV_STATS")) {  // diagnostic counters of a VPET_UNION_STATS build (scan_kernels.cuh)
     unsigned long long u[2] = {0, 0};
     CK(cudaMemcpy(u, static_cast<unsigned long long*>(ctx->work.p) + 2, 16, cudaMemcpyDeviceToHost));
-    fprintf(stderr, "diag counters: work[2] %llu, work[3] %llu (union stats: evaluated / alive voxel-lane tiles; push stats: pushes in work[3])\n", u[0], u[1]);
+    unsigned long long w1 = 0;
+    CK(cudaMemcpy(&w1, static_cast<unsigned long long*>(ctx->work.p) + 1, 8, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "diag counters: work[1]>>32 %llu, work[2] %llu, work[3] %llu (union: evaluated / alive voxel-lane "
+            "tiles; push: pushes in work[3]; trav: super-tiles checked / passed / tiles loaded)\n", w1 >> 32, u[0], u[1]);
   }
   S.frame_updates = h_work[0];
   S.bound_updates = h_work[1];

@@ -942,6 +942,9 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       // super-tile bound
       const uint32_t sbx_a = bbuf_a + cur * uint32_t(BXF) * 4u;  // shared address of the boxes
       bool alive = halive && box_alive<LP, R, DIST>(V, SmemSrc{sbx_a}, bwork);
+#ifdef VPET_TRAV_STATS
+      if (tid == 0) atomicAdd(p.work + 1, 1ull << 32);  // super-tiles bound-checked (high word of bound_work)
+#endif
       if (!__syncthreads_or(alive)) continue;
       // tile bounds -> per-warp masks
       const uint64_t t0 = s * kSuper;
@@ -985,6 +988,13 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       for (int w = 0; w < NW; ++w) cm |= wmask[w];
       const uint32_t mym = wmask[wid];
       const uint32_t nal = __popc(cm);
+#ifdef VPET_TRAV_STATS
+      // diagnostic: super-tiles that passed the super bound (per CTA) and tiles loaded (per CTA)
+      if (tid == 0) {
+        atomicAdd(p.work + 2, 1ull);
+        atomicAdd(p.work + 3, 1ull * nal);
+      }
+#endif
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         uint32_t m = cm;

@@ -19,6 +19,7 @@ VARIANTS = {
     "pair": ("VPET_PAIR=1",),
     "union": ("VPET_UNION_STATS=1",),
     "pushstats": ("VPET_PUSH_STATS=1",),
+    "trav": ("VPET_TRAV_STATS=1",),
     "nocontig": ("VPET_WARP_CONTIG=0",),
     "morton": ("VPET_HILBERT=0",),
     "hbank": ("VPET_HILBERT=1", "VPET_HILBERT_VOX=0"),
