@@ -42,9 +42,19 @@ constexpr int NT = VPET_NT;   // threads per CTA (the warps of a CTA share tile 
 constexpr int NW = NT / 32;
 constexpr int NST = VPET_NST;  // TMA ring stages
 #ifndef VPET_CH
-#define VPET_CH 16
+#define VPET_CH 0
 #endif
-constexpr int CH = VPET_CH;  // frames per pruning chunk (multiple of 4)
+constexpr int CH = VPET_CH;  // frames per pruning chunk of a draw evaluation (multiple of 4); 0 = LP (one chunk)
+// Chunk of a draw evaluation: the whole row when two voxels share a lane (LP <= 48): a row is then
+// evaluated for 64 voxels, one of which nearly always keeps it alive past a 16-frame chunk (rows ran
+// 31 of 36 frames on the TB volume), so the intermediate votes cost more than they save (scan -9.5 %
+// with 12-frame bound chunks).  16 frames for the one-voxel-per-lane layouts.
+template <int LP>
+__host__ __device__ constexpr int chd() { return CH > 0 ? CH : (LP <= 48 ? LP : 16); }
+#ifndef VPET_CHB
+#define VPET_CHB 12
+#endif
+constexpr int CHB = VPET_CHB;  // frames per pruning chunk of a box lower bound (multiple of 4)
 constexpr int T = kTile;
 #ifndef VPET_REFRESH
 #define VPET_REFRESH 0  // pull tau_glob every VPET_REFRESH + 1 super-tiles
@@ -387,7 +397,8 @@ struct GmemSrc {
 template <int LP, int R, int DIST, int C, class Src>
 __device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const Src sr, Acc (&acc)[R]) {
 #pragma unroll
-  for (int q = C * CH; q < ((C + 1) * CH < LP ? (C + 1) * CH : LP); q += 4) {
+  constexpr int CD = chd<LP>();
+  for (int q = C * CD; q < ((C + 1) * CD < LP ? (C + 1) * CD : LP); q += 4) {
     const float4 s4 = sr.ld(q);
     const float2 sa = make_float2(s4.x, s4.y);
     const float2 sc = make_float2(s4.z, s4.w);
@@ -413,7 +424,7 @@ __device__ __forceinline__ void dist_chunk(const Voxels<LP, R>& V, const Src sr,
 template <int LP, int R, int DIST, int C, class Src>
 __device__ __forceinline__ void bound_chunk(const Voxels<LP, R>& V, const Src lo, const Src hi, Acc (&acc)[R]) {
 #pragma unroll
-  for (int q = C * CH; q < ((C + 1) * CH < LP ? (C + 1) * CH : LP); q += 4) {
+  for (int q = C * CHB; q < ((C + 1) * CHB < LP ? (C + 1) * CHB : LP); q += 4) {
     const float4 l4 = lo.ld(q);
     const float4 h4 = hi.ld(q);
     const float2 la = make_float2(l4.x, l4.y), lc = make_float2(l4.z, l4.w);
@@ -449,13 +460,14 @@ __device__ __forceinline__ bool any_alive(const Voxels<LP, R>& V, const Acc (&ac
 // Unrolled chunk loop with warp-uniform early exit after each chunk.
 template <int LP, int R, int DIST, bool BOUND, int C>
 struct Chunks {
-  static constexpr int NCH = (LP + CH - 1) / CH;
+  static constexpr int CHX = BOUND ? CHB : chd<LP>();
+  static constexpr int NCH = (LP + CHX - 1) / CHX;
   template <class Src>
   __device__ __forceinline__ static bool run(const Voxels<LP, R>& V, const Src a, const Src b, Acc (&acc)[R],
                                              unsigned long long& work, bool noprune) {
     if (BOUND) bound_chunk<LP, R, DIST, C>(V, a, b, acc);
     else dist_chunk<LP, R, DIST, C>(V, a, acc);
-    work += uint64_t(((C + 1) * CH < LP ? (C + 1) * CH : LP) - C * CH) * R;
+    work += uint64_t(((C + 1) * CHX < LP ? (C + 1) * CHX : LP) - C * CHX) * R;
     if (!any_alive<LP, R>(V, acc, noprune)) return false;
     if constexpr (C + 1 < NCH) return Chunks<LP, R, DIST, BOUND, C + 1>::run(V, a, b, acc, work, noprune);
     return true;
@@ -519,7 +531,7 @@ template <int LP, int R, int DIST, bool COUNT, bool SH = false>
 __device__ __forceinline__ void eval_pair(const ScanParams& p, Voxels<LP, R>& V, const SmemSrc sa, uint64_t ia,
                                           const SmemSrc sb, uint64_t ib, uint32_t part, unsigned long long& work,
                                           uint32_t htop_s = 0) {
-  constexpr int NCH = (LP + CH - 1) / CH;
+  constexpr int NCH = (LP + chd<LP>() - 1) / chd<LP>();
   Acc aa[R], ab[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -528,7 +540,7 @@ __device__ __forceinline__ void eval_pair(const ScanParams& p, Voxels<LP, R>& V,
   }
   dist_chunk<LP, R, DIST, 0>(V, sa, aa);
   dist_chunk<LP, R, DIST, 0>(V, sb, ab);
-  unsigned long long w = 2ull * uint64_t((CH < LP ? CH : LP)) * R;
+  unsigned long long w = 2ull * uint64_t((chd<LP>() < LP ? chd<LP>() : LP)) * R;
   bool ga = any_alive<LP, R>(V, aa, !p.prune);
   bool gb = any_alive<LP, R>(V, ab, !p.prune);
   if constexpr (NCH > 1) {

@@ -30,6 +30,14 @@ VARIANTS = {
     "nst3": ("VPET_NST=3",),
     "ch12": ("VPET_CH=12",),
     "ch20": ("VPET_CH=20",),
+    "ch24": ("VPET_CH=24",),
+    "ch36": ("VPET_CH=36",),
+    "ch36b12": ("VPET_CH=36", "VPET_CHB=12"),
+    "ch36b16": ("VPET_CH=36", "VPET_CHB=16"),
+    "ch36b20": ("VPET_CH=36", "VPET_CHB=20"),
+    "old16": ("VPET_CH=16", "VPET_CHB=16"),
+    "chb8": ("VPET_CHB=8",),
+    "c3ch32": ("VPET_CH=32", "VPET_CHB=12"),
     "tr3acc2": ("VPET_TREFRESH=3", "VPET_ACC2=1"),
     "npc3": ("VPET_NPC=3",),
     "npc5": ("VPET_NPC=5",),
