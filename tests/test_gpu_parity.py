@@ -357,3 +357,24 @@ def test_continuous_phantom_parity(ell):
     o, _ = run_oracle(sub)
     rep = compare(g, o)
     assert rep["matched"] >= sub.J - 2
+
+
+def test_two_contexts_one_process(tb_small, rt_small):
+    """Two live contexts in one process (different models, frame counts and shared-memory sizes of the
+    certification: n = 18 vs n = 400): per-device kernel attributes and per-context buffers do not
+    interfere; each equals its own single-context run."""
+    from paper_2603_14859_b200 import AbcContext
+    a_ref, _ = run_gpu(tb_small)
+    b_prob = rt_small.replace(n_accept=400)
+    b_ref, _ = run_gpu(b_prob)
+    ca = AbcContext(**tb_small.ctx_kwargs)
+    tb_small.setup(ca)
+    cb = AbcContext(**b_prob.ctx_kwargs)
+    b_prob.setup(cb)
+    for _ in range(2):
+        ra = ca.run_voxels(tb_small.tacs)
+        rb = cb.run_voxels(b_prob.tacs)
+        for k in a_ref:
+            np.testing.assert_array_equal(np.nan_to_num(ra[k]), np.nan_to_num(a_ref[k]), err_msg=k)
+        for k in b_ref:
+            np.testing.assert_array_equal(np.nan_to_num(rb[k]), np.nan_to_num(b_ref[k]), err_msg=k)

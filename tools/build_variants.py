@@ -36,6 +36,10 @@ VARIANTS = {
     "ch36b16": ("VPET_CH=36", "VPET_CHB=16"),
     "ch36b20": ("VPET_CH=36", "VPET_CHB=20"),
     "old16": ("VPET_CH=16", "VPET_CHB=16"),
+    "super4": ("VPET_SUPER=4",),
+    "super16": ("VPET_SUPER=16",),
+    "nst3b": ("VPET_NST=3",),
+    "tile16": ("VPET_TILE=16",),
     "chb8": ("VPET_CHB=8",),
     "c3ch32": ("VPET_CH=32", "VPET_CHB=12"),
     "tr3acc2": ("VPET_TREFRESH=3", "VPET_ACC2=1"),
