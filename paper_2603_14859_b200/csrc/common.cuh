@@ -252,6 +252,12 @@ struct VoxelOrderParams {
   size_t sort_temp_bytes;
 };
 size_t voxel_sort_temp_bytes(uint64_t J);
+// Stable LSD radix sort of (u64 key, u32 value) pairs on key bits [lo_bit, hi_bit) (radix.cu).
+// keys / keys_alt are overwritten (ping-pong); the sorted values land in vals_out.
+size_t radix_temp_bytes(uint64_t n);
+cudaError_t radix_sort_pairs(void* temp, size_t temp_bytes, unsigned long long* keys, unsigned long long* keys_alt,
+                             const uint32_t* vals_in, uint32_t* vals_out, uint64_t n, int lo_bit, int hi_bit,
+                             cudaStream_t st, uint32_t* launches);
 cudaError_t launch_voxel_order(const VoxelOrderParams& p, cudaStream_t st, uint32_t* launches);
 
 // Rigorous bound on |D32 - D| for the FP32 pass:

@@ -7,7 +7,6 @@
 // boxes of tiles of T draws (and of super-tiles of ST tiles) are tight and give exact lower
 // bounds on the FP32 discrepancy of every draw inside them (scan_tree.cu).  The order only
 // changes which draws are looked at first; selection is by (D, original index) keys.
-#include <cub/cub.cuh>
 
 #include <cstdlib>
 
@@ -545,29 +544,18 @@ __global__ void __launch_bounds__(256) voxel_key_kernel(const VoxelOrderParams p
 
 }  // namespace
 
-size_t voxel_sort_temp_bytes(uint64_t J) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, int(J), 0, kVoxBits);
-  return bytes;
-}
+size_t voxel_sort_temp_bytes(uint64_t J) { return radix_temp_bytes(J); }
 
 cudaError_t launch_voxel_order(const VoxelOrderParams& p, cudaStream_t st, uint32_t* launches) {
   voxel_key_kernel<<<148 * 4, 256, 0, st>>>(p);
-  size_t tb = p.sort_temp_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(p.sort_temp, tb, p.keys, p.keys_alt, p.vals, p.vorder, int(p.J), 0,
-                                                  kVoxBits, st);
-  *launches += 5;
+  *launches += 1;
+  cudaError_t e = radix_sort_pairs(p.sort_temp, p.sort_temp_bytes, p.keys, p.keys_alt, p.vals, p.vorder, p.J, 0,
+                                   kVoxBits, st, launches);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-size_t order_sort_temp_bytes(uint64_t N) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                  (const uint32_t*)nullptr, (uint32_t*)nullptr, int(N), 0, kNPC * kMBits);
-  return bytes;
-}
+size_t order_sort_temp_bytes(uint64_t N) { return radix_temp_bytes(N); }
 
 cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launches) {
   frame_stats_kernel<<<p.L, 1024, 0, st>>>(p);
@@ -581,15 +569,14 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
     proj_minmax_kernel<<<148 * 4, 256, 0, st>>>(p);
     key_kernel<<<148 * 8, 256, 0, st>>>(p);
     *launches += 4;
-    size_t tb = p.sort_temp_bytes;
-    // the lowest 8 key bits (the two finest Morton levels of each axis) are not sorted: one radix
-    // pass less, same scan time (measured: 0 / 8 / 16 bits -> scan 19.6 / 19.5 / 20.3 ms); the
-    // order is free.  Tuning knob VPET_SORT_LO.
+    // the lowest 8 key bits (the two finest levels of the curve) are not sorted: one radix pass
+    // less, same scan time (Morton, measured: 0 / 8 / 16 bits -> scan 19.6 / 19.5 / 20.3 ms; with
+    // the Hilbert order 24 unsorted bits double the scan); the order is free.
+    // Tuning knob VPET_SORT_LO.
     static const int lo_bit = getenv("VPET_SORT_LO") ? atoi(getenv("VPET_SORT_LO")) : 8;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(p.sort_temp, tb, p.keys, p.keys_alt, p.vals, p.order, int(p.N), lo_bit,
-                                                    kNPC * kMBits, st);
+    cudaError_t e = radix_sort_pairs(p.sort_temp, p.sort_temp_bytes, p.keys, p.keys_alt, p.vals, p.order, p.N, lo_bit,
+                                     kNPC * kMBits, st, launches);
     if (e != cudaSuccess) return e;
-    *launches += 4;  // onesweep: histogram + passes (approximate count of CUB launches)
   } else {
     q.order = nullptr;
   }
