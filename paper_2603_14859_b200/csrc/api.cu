@@ -100,6 +100,7 @@ struct abc_ctx {
   cudaStream_t copy = nullptr;       // host->device TAC copies, overlapped with the bank / order stages
   cudaEvent_t tacs_ready = nullptr;
   bool ev_ok = false;
+  int num_sms = 148;
 };
 
 namespace {
@@ -415,6 +416,7 @@ abc_status abc_init(const abc_config* cfg, abc_ctx** out) {
   if (!c) return ABC_E_NOMEM;
   c->cfg = *cfg;
   c->dev = cfg->device;
+  if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess) c->num_sms = 148;
   c->N = N;
   c->M = cfg->n_models;
   c->P = family_width(cfg->model[0].kind);
@@ -604,7 +606,18 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   uint32_t nparts = 1;
   // parts share the draws of a voxel between SMs; each keeps its own K candidates, so large n uses
   // fewer parts (certification holds all parts' candidates of a voxel in shared memory)
-  if (tree && !eps) nparts = K <= 512 ? 6u : (2 * K <= kLargeMaxCand ? 2u : 1u);
+  // The parts also balance the persistent scan over the SMs: with few voxel tiles per CTA slot
+  // more parts keep every SM busy, with many the parts only duplicate heap fills and threshold
+  // traffic.  Measured best on the TB phantom (CTA slots = SMs x 8): 6 parts at 0.96 voxel tiles per
+  // slot (1/32 slab set), 4 at 3.7 (1/8), 3 at 29 (the whole volume: 361 -> 319 ms vs 6 parts).
+  if (tree && !eps) {
+    if (K <= 512) {
+      const double tiles_per_slot = double((J + 127) / 128) / double(std::max(1, ctx->num_sms) * 8);
+      nparts = tiles_per_slot < 2.0 ? 6u : (tiles_per_slot < 10.0 ? 4u : 3u);
+    } else {
+      nparts = 2 * K <= kLargeMaxCand ? 2u : 1u;
+    }
+  }
   if (tree && eps) nparts = 6u;
   if (const char* e = getenv("VPET_NPARTS")) nparts = uint32_t(std::max(1, atoi(e)));  // tuning knob
   // hyper-tiles of hs super-tiles: the unit of the work split and of the best-first order; at most
