@@ -17,6 +17,8 @@ VARIANTS = {
     "tr4": ("VPET_TREFRESH=4",),
     "hinl": ("VPET_HEAP_INLINE=1",),
     "pair": ("VPET_PAIR=1",),
+    "hsort512": ("VPET_HSORTMAX=512",),
+    "qorder0": ("VPET_QORDER=0",),
     "union": ("VPET_UNION_STATS=1",),
     "pushstats": ("VPET_PUSH_STATS=1",),
     "trav": ("VPET_TRAV_STATS=1",),
