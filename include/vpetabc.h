@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define VPETABC_ABI_VERSION 1
+#define VPETABC_ABI_VERSION 2  /* 2: abc_stats.n_fallback_exact, abc_reduce_accepted, n <= 15360 */
 #define ABC_MAX_P 8       /* parameter columns per draw (2TCM family uses 5, RT family 7) */
 #define ABC_MAX_MODELS 4  /* M */
 #define ABC_MAX_L 128     /* frames per TAC */

@@ -14,6 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VPET_LIB") or os.path.join(_HERE, "libvpetabc.so")  # VPET_LIB: tuning builds only
 
+ABI_VERSION = 2  # include/vpetabc.h VPETABC_ABI_VERSION
 MAX_P = 8
 MAX_MODELS = 4
 MAX_L = 128
@@ -104,6 +105,8 @@ def load_library(path: str = LIB_PATH):
     L.abc_destroy.restype = None
     L.abc_abi_version.restype = C.c_uint32
     assert C.sizeof(Config) == 376, C.sizeof(Config)
+    if L.abc_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"{path}: ABI version {L.abc_abi_version()} != {ABI_VERSION} of this binding (rebuild)")
     _lib = L
     return L
 

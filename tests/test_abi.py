@@ -28,7 +28,7 @@ def test_library_loads_and_exports_every_header_symbol():
     for s in header_symbols():
         assert hasattr(lib, s), s
     assert set(header_symbols()) == set(_abi.SYMBOLS)
-    assert lib.abc_abi_version() == 1
+    assert lib.abc_abi_version() == 2
 
 
 def test_struct_layouts():

@@ -17,6 +17,8 @@ VARIANTS = {
     "tr4": ("VPET_TREFRESH=4",),
     "hinl": ("VPET_HEAP_INLINE=1",),
     "pair": ("VPET_PAIR=1",),
+    "nt128": ("VPET_NT=128",),
+    "nt32": ("VPET_NT=32",),
     "hsort512": ("VPET_HSORTMAX=512",),
     "qorder0": ("VPET_QORDER=0",),
     "union": ("VPET_UNION_STATS=1",),
