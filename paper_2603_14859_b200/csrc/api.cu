@@ -81,6 +81,8 @@ struct abc_ctx {
   bool dirty = true;
   uint32_t G = 0, GF = 0;
   DevBuf d_finv;  // [L] 1 / frame duration (the bank multiplies instead of dividing)
+  DevBuf d_s0;    // [L] S_f(0) of the PWL grid (irreversible 2TCM draws)
+  bool have_s0 = false;
   DevBuf d_fdur, d_fs, d_fe, d_favg, d_w, d_wsc, d_gt, d_gc, d_gframe, d_gcode, d_ft, d_fc, d_fframe;
   // work buffers
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
@@ -175,6 +177,8 @@ double feng_frame_integral(const double* b, double ts, double te) {
   return b[0] * tint - (b[1] + b[2]) * G(k1, ts, te) + b[1] * G(b[4], ts, te) + b[2] * G(b[5], ts, te);
 }
 
+Tables make_tables(const abc_ctx* c, uint32_t LS);
+
 abc_status build_tables(abc_ctx* ctx) {
   if (!ctx->dirty) return ABC_OK;
   const uint32_t L = ctx->L;
@@ -257,6 +261,17 @@ abc_status build_tables(abc_ctx* ctx) {
   CK(cudaMemcpy(ctx->d_prior.p, &ctx->prior, sizeof(PriorDev), cudaMemcpyHostToDevice));
   ctx->G = uint32_t(gt.size());
   ctx->GF = uint32_t(ft.size());
+  ctx->have_s0 = false;
+  if (ctx->input_kind == ABC_INPUT_PWL && ctx->cfg.model[0].kind <= ABC_2TCM_REV) {
+    CK(ctx->d_s0.ensure(sizeof(double) * L));
+    CK(cudaMemset(ctx->d_s0.p, 0, sizeof(double) * L));
+    Tables T = make_tables(ctx, (L + 3) & ~3u);
+    T.s0 = nullptr;
+    launch_s0_table(T, ctx->d_s0.as<double>(), nullptr);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());  // the context's stream does not synchronise with the legacy stream
+    ctx->have_s0 = true;
+  }
   ctx->dirty = false;
   return ABC_OK;
 }
@@ -284,6 +299,7 @@ Tables make_tables(const abc_ctx* c, uint32_t LS) {
   T.noise_ell = c->noise_ell;
   T.noise_lam = c->noise_lam;
   for (int k = 0; k < 6; ++k) T.fb[k] = c->feng[k];
+  T.s0 = c->have_s0 ? c->d_s0.as<double>() : nullptr;
   return T;
 }
 
@@ -1346,7 +1362,7 @@ void abc_destroy(abc_ctx* ctx) {
                      &ctx->env_idx, &ctx->env_t, &ctx->env_q, &ctx->proj, &ctx->pat_ab,
                      &ctx->fb_tau, &ctx->cl_d, &ctx->cl_i, &ctx->cl_cnt, &ctx->fb2_list, &ctx->fb2_len};
   for (DevBuf* b : bufs2) b->release();
-  DevBuf* bufs[] = {&ctx->d_finv, &ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
+  DevBuf* bufs[] = {&ctx->d_finv, &ctx->d_s0, &ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,
                     &ctx->bank,   &ctx->bankp, &ctx->var,    &ctx->perm,   &ctx->wsp,        &ctx->heap,
                     &ctx->heap_cnt, &ctx->tacs, &ctx->fb_list, &ctx->fb_len, &ctx->work,     &ctx->hd,

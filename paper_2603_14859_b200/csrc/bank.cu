@@ -111,6 +111,79 @@ __device__ void sim_2tcm_pwl(const Tables& T, const DrawId& D, double a1, double
   if (fa.cur >= 0) flush(fa.cur);
 }
 
+// ---- irreversible 2TCM (k4 = 0, so a1 = 0): the a1 = 0 frame integrals S_f(0) do not depend on the
+// draw; they are precomputed once per grid (s0_table_kernel, the same FP64 operations as the a1
+// half of sim_2tcm_pwl) and only the a2 recurrence runs per draw ----
+template <bool NZ>
+__device__ void sim_2tcm_pwl_irr(const Tables& T, const DrawId& D, double a2, double c1, double c2, double Vb,
+                                 float* out) {
+  double I2 = 0.0;
+  Phi Q0{}, Q1{};
+  FrameAcc fa;
+  auto flush = [&](int f) {
+    double v = ((1.0 - Vb) * (c1 * T.s0[f] + c2 * fa.B) + Vb * T.favg_in[f]) * T.finv[f];
+    out[f] = emit<NZ>(T, D, f, v);
+  };
+  for (uint32_t k = 0; k + 1 < T.G; ++k) {
+    double t0 = T.gt[k], t1 = T.gt[k + 1];
+    double h = t1 - t0;
+    double ck = T.gc[k], ck1 = T.gc[k + 1];
+    int f = T.gframe[k];
+    const uint32_t code = T.gcode[k];
+    const uint32_t slot = code & 3u;
+    if (code & 0x80u) {
+      Phi nq = phi_all(a2 * h);
+      if (slot == 0) Q0 = nq; else Q1 = nq;
+    }
+    auto body = [&](const Phi& q) {
+      double dc = ck1 - ck;
+      double s2 = h * q.p1 * I2 + h * h * (ck1 * q.ps - dc * q.om);
+      if (f != fa.cur) {
+        if (fa.cur >= 0) flush(fa.cur);
+        fa.cur = f;
+        fa.B = 0.0;
+      }
+      fa.B += s2;
+      I2 = q.e * I2 + h * (ck * q.ch + ck1 * q.ps);
+    };
+    if (slot == 0) body(Q0);
+    else body(Q1);
+  }
+  if (fa.cur >= 0) flush(fa.cur);
+}
+
+__global__ void s0_table_kernel(const Tables T, double* s0) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double I1 = 0.0;
+  Phi P0{}, P1{};
+  int cur = -1;
+  double A = 0.0;
+  const double a1 = 0.0;
+  for (uint32_t k = 0; k + 1 < T.G; ++k) {
+    double t0 = T.gt[k], t1 = T.gt[k + 1];
+    double h = t1 - t0;
+    double ck = T.gc[k], ck1 = T.gc[k + 1];
+    int f = T.gframe[k];
+    const uint32_t code = T.gcode[k];
+    const uint32_t slot = code & 3u;
+    if (code & 0x80u) {
+      Phi np = phi_all(a1 * h);
+      if (slot == 0) P0 = np; else P1 = np;
+    }
+    const Phi& p = slot == 0 ? P0 : P1;
+    double dc = ck1 - ck;
+    double s1 = h * p.p1 * I1 + h * h * (ck1 * p.ps - dc * p.om);
+    if (f != cur) {
+      if (cur >= 0) s0[cur] = A;
+      cur = f;
+      A = 0.0;
+    }
+    A += s1;
+    I1 = p.e * I1 + h * (ck * p.ch + ck1 * p.ps);
+  }
+  if (cur >= 0) s0[cur] = A;
+}
+
 // ---- Feng input: closed forms of e^{-a t} (x) {e^{-k t}, t e^{-k t}} and their integrals ----
 __device__ inline double convE(double a, double k, double t) {
   double mn = fmin(a, k);
@@ -240,6 +313,7 @@ __global__ void __launch_bounds__(128) bank_kernel(const BankParams p, const Pri
     double c1 = K1 * (k3 + k4 - a1) / den;
     double c2 = K1 * (a2 - k3 - k4) / den;
     if (T.feng) sim_2tcm_feng<NZ>(T, D, a1, a2, c1, c2, Vb, out);
+    else if (a1 == 0.0 && T.s0) sim_2tcm_pwl_irr<NZ>(T, D, a2, c1, c2, Vb, out);
     else sim_2tcm_pwl<NZ>(T, D, a1, a2, c1, c2, Vb, out);
   } else if (kind == ABC_MRTM) {
     sim_mrtm<NZ>(T, D, th[0], th[1], th[2], out);
@@ -261,6 +335,8 @@ void launch_bank(const BankParams& p, const PriorDev& prior, cudaStream_t st) {
   if (p.T.noise_ell != 0.0) bank_kernel<true><<<unsigned(blocks), 128, 0, st>>>(p, prior);
   else bank_kernel<false><<<unsigned(blocks), 128, 0, st>>>(p, prior);
 }
+
+void launch_s0_table(const Tables& T, double* s0, cudaStream_t st) { s0_table_kernel<<<1, 32, 0, st>>>(T, s0); }
 
 void launch_fill_u32(uint32_t* p, uint32_t v, uint64_t n, cudaStream_t st) {
   fill_u32_kernel<<<148, 256, 0, st>>>(p, v, n);

@@ -190,6 +190,9 @@ struct Tables {
   double fb[6];
   // simulated-draw noise (abc_set_sim_noise): ell = 0 disables
   double noise_ell, noise_lam;
+  // [L] S_f(0) = frame integrals of the rate-0 convolution on the coarse grid (PWL input): the
+  // draw-independent half of an irreversible 2TCM draw (launch_s0_table); nullptr = not available
+  const double* s0;
 };
 
 struct BankParams {
@@ -199,6 +202,7 @@ struct BankParams {
 };
 
 void launch_bank(const BankParams& p, const PriorDev& prior, cudaStream_t st);
+void launch_s0_table(const Tables& T, double* s0, cudaStream_t st);
 
 struct OrderParams {
   const float* bank;  // [N][LS]
