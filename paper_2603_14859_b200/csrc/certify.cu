@@ -886,6 +886,140 @@ __global__ void reduce_list_kernel(const ReduceParams p, const IdxT* idx, const 
   }
 }
 
+// ---- K4, thread per voxel (n <= 32, the accepted lists of the K3/K4 split) -------------------
+// One thread summarises one voxel: per column, the accepted draws' values (the preferred model's;
+// +inf for the others and for the padding) go to the thread's own 8-byte slots of shared memory
+// ([a][thread]: conflict-free), come back into registers, are sorted by a fixed 32-element bitonic network
+// (static register indices, fmin/fmax) and written back for the type-7 order statistics.  Sums run
+// sequentially in accepted-list order, in FP64.  Roughly a tenth of the warp-per-voxel version's
+// warp instructions (a warp summarises 32 voxels at once instead of one).
+constexpr int kRT = 128;  // threads per block of the thread-per-voxel reduction
+
+template <typename T>
+__device__ __forceinline__ void sort32_regs(T (&r)[32]) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const T a = r[i], b = r[l];
+          const T lo = a < b ? a : b, hi = a < b ? b : a;
+          if ((i & k) == 0) { r[i] = lo; r[l] = hi; } else { r[i] = hi; r[l] = lo; }
+        }
+      }
+    }
+  }
+}
+
+// this thread's 32 column entries live in its own 8-byte slots of smem_d[a][thread] (an FP32
+// value in the first half of the slot: FP32 and FP64 columns never overlap another thread's)
+template <typename T>
+__device__ __forceinline__ T& col_at(double* slot0, uint32_t a) {
+  return *reinterpret_cast<T*>(slot0 + a * kRT);
+}
+
+template <typename T>
+__device__ __forceinline__ void column_summary(double* col, uint32_t c, double sum, double ss, float& mean, float& sd,
+                                               float (&q3)[3]) {
+  // first c entries finite
+  T r[32];
+#pragma unroll
+  for (int a = 0; a < 32; ++a) r[a] = col_at<T>(col, a);
+  sort32_regs<T>(r);
+#pragma unroll
+  for (int a = 0; a < 32; ++a) col_at<T>(col, a) = r[a];
+  const double mu = sum / double(c);
+  mean = float(mu);
+  sd = c >= 2 ? float(sqrt(ss / double(c - 1))) : __int_as_float(0x7fc00000);
+  const double qs[3] = {0.025, 0.5, 0.975};
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const double h = double(c - 1) * qs[t];
+    const uint32_t lo = uint32_t(floor(h));
+    const double xl = double(col_at<T>(col, lo));
+    q3[t] = float(lo + 1 < c ? xl + (h - double(lo)) * (double(col_at<T>(col, lo + 1)) - xl) : xl);
+  }
+}
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kRT) reduce_thread_kernel(const ReduceParams p, const IdxT* __restrict__ idx,
+                                                             const double* __restrict__ dist, uint32_t n_acc, int* bad) {
+  __shared__ double smem_d[32 * kRT];  // per-thread columns [a][thread] (FP64 for K_i, FP32 aliases it)
+  if (p.bad && *p.bad) return;
+  const uint64_t v = uint64_t(blockIdx.x) * kRT + threadIdx.x;
+  if (v >= p.J) return;
+  const uint32_t n = p.n, M = p.prior.M;
+  const abc_result& o = p.out;
+  const IdxT* li = idx + v * n_acc;
+  uint32_t cnt[ABC_MAX_MODELS] = {0, 0, 0, 0};
+  for (uint32_t a = 0; a < n; ++a) {
+    uint64_t i = uint64_t(li[a]);
+    if (i >= p.N) {
+      atomicExch(bad, 1);
+      i = 0;
+    }
+    cnt[model_index(p.prior, i)] += 1;
+    if (o.acc_idx) o.acc_idx[v * n + a] = i;
+    if (o.acc_dist && dist) o.acc_dist[v * n + a] = dist[v * n_acc + a];
+  }
+  int pref = 0;
+  for (uint32_t m = 1; m < M; ++m)
+    if (cnt[m] > cnt[pref]) pref = int(m);
+  for (uint32_t m = 0; m < M; ++m) {
+    if (o.count) o.count[v * M + m] = cnt[m];
+    if (o.prob) o.prob[v * M + m] = float(double(cnt[m]) / double(n));
+  }
+  if (o.preferred) o.preferred[v] = pref;
+  const int kind = p.prior.m[pref].kind;
+  const uint32_t c = cnt[pref];
+  const bool tcm = kind <= ABC_2TCM_REV;
+  const float NANF = __int_as_float(0x7fc00000);
+  double* col = smem_d + threadIdx.x;  // this thread's slots [a * kRT]
+  for (uint32_t k = 0; k <= p.P; ++k) {  // column P = K_i
+    const bool is_ki = (k == p.P);
+    const bool exists = c > 0 && (is_ki ? tcm : column_exists(kind, k));
+    float mean = NANF, sd = NANF, q3[3] = {NANF, NANF, NANF};
+    if (exists) {
+      const uint32_t blk = (is_ki || k < 4) ? 0u : 1u;
+      double sum = 0.0;
+      for (uint32_t a = 0; a < 32; ++a) {
+        double x = __longlong_as_double(0x7ff0000000000000ll);
+        if (a < n) {
+          const uint64_t i = uint64_t(li[a]) < p.N ? uint64_t(li[a]) : 0ull;
+          if (model_index(p.prior, i) == pref) {
+            float th[ABC_MAX_P];
+            theta_block(p.prior, i, pref, blk, th);
+            x = is_ki ? double(th[0]) * double(th[2]) / (double(th[1]) + double(th[2])) : double(th[k]);
+            sum += x;
+          }
+        }
+        if (is_ki) col_at<double>(col, a) = x;
+        else col_at<float>(col, a) = float(x);
+      }
+      const double mu = sum / double(c);
+      double ss = 0.0;
+      for (uint32_t a = 0; a < n; ++a) {
+        const double x = is_ki ? col_at<double>(col, a) : double(col_at<float>(col, a));
+        if (x != __longlong_as_double(0x7ff0000000000000ll)) ss += (x - mu) * (x - mu);
+      }
+      if (is_ki) column_summary<double>(col, c, sum, ss, mean, sd, q3);
+      else column_summary<float>(col, c, sum, ss, mean, sd, q3);
+    }
+    if (is_ki) {
+      if (o.ki_mean) o.ki_mean[v] = mean;
+      if (o.ki_sd) o.ki_sd[v] = sd;
+      if (o.ki_q) for (int t = 0; t < 3; ++t) o.ki_q[v * 3 + t] = q3[t];
+    } else {
+      if (o.mean) o.mean[v * p.P + k] = mean;
+      if (o.sd) o.sd[v * p.P + k] = sd;
+      if (o.q) for (int t = 0; t < 3; ++t) o.q[(v * p.P + k) * 3 + t] = q3[t];
+    }
+  }
+}
+
 uint32_t next_pow2(uint32_t x) {
   uint32_t p = 1;
   while (p < x) p <<= 1;
@@ -1070,6 +1204,13 @@ void launch_eps_reduce(const EpsReduceParams& p, cudaStream_t st) {
 template <typename IdxT>
 static cudaError_t launch_reduce_list_t(const ReduceParams& p, const IdxT* idx, const double* dist, uint32_t n_acc,
                                         int* bad, cudaStream_t st) {
+  // n <= 32: thread per voxel (reduce_thread_kernel); else warp per voxel (reduce_list_kernel)
+  static const bool thread_env = getenv("VPET_REDUCE_THREAD") ? atoi(getenv("VPET_REDUCE_THREAD")) != 0 : true;  // tuning knob
+  if (thread_env && p.n <= 32) {
+    const uint64_t blocks = (p.J + kRT - 1) / kRT;
+    reduce_thread_kernel<IdxT><<<unsigned(blocks > 0 ? blocks : 1), kRT, 0, st>>>(p, idx, dist, n_acc, bad);
+    return cudaGetLastError();
+  }
   uint32_t np2 = next_pow2(p.n);
   if (np2 < 32) np2 = 32;
   const size_t per_warp = size_t(np2) * 12;
