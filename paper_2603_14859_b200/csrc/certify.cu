@@ -18,15 +18,29 @@
 namespace vpet {
 namespace {
 
-__device__ __forceinline__ double exact_distance_c(const float* y, const float* s, const float* w, uint32_t L,
+// FP64 distance of one candidate, term by term in acquisition frame order as the oracle computes
+// it (no contraction).  The bank row is read as float4 (rows are LS = L rounded up to 4 floats,
+// 16-B aligned; w is a 16-B aligned device array): a quarter of the divergent row loads.
+__device__ __forceinline__ double exact_distance_v(const float* y, const float* s, const float* w, uint32_t L,
                                                    int dist) {
+  const float4* s4 = reinterpret_cast<const float4*>(s);
+  const float4* w4 = reinterpret_cast<const float4*>(w);
   double D = 0.0;
-#pragma unroll 8
-  for (uint32_t f = 0; f < L; ++f) {
-    double d = __dsub_rn(double(__ldg(y + f)), double(__ldg(s + f)));
-    double t = (dist == ABC_DIST_L1) ? fabs(d) : __dmul_rn(d, d);
-    D = __dadd_rn(D, __dmul_rn(double(__ldg(w + f)), t));
+  auto term = [&](float yv, float sv, float wv) {
+    const double d = __dsub_rn(double(yv), double(sv));
+    const double t = (dist == ABC_DIST_L1) ? fabs(d) : __dmul_rn(d, d);
+    D = __dadd_rn(D, __dmul_rn(double(wv), t));
+  };
+  uint32_t f = 0;
+#pragma unroll 2
+  for (; f + 4 <= L; f += 4) {
+    const float4 sv = __ldg(s4 + f / 4), wv = __ldg(w4 + f / 4);
+    term(__ldg(y + f), sv.x, wv.x);
+    term(__ldg(y + f + 1), sv.y, wv.y);
+    term(__ldg(y + f + 2), sv.z, wv.z);
+    term(__ldg(y + f + 3), sv.w, wv.w);
   }
+  for (; f < L; ++f) term(__ldg(y + f), __ldg(s + f), __ldg(w + f));
   return D;
 }
 
@@ -422,7 +436,7 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
       __syncwarp();
       for (uint32_t a = lane; a < Kp; a += 32) {
         if (a < nc) {
-          cd[a] = exact_distance_c(y, p.bank + uint64_t(ci[a]) * p.LS, p.w, p.L, p.dist);
+          cd[a] = exact_distance_v(y, p.bank + uint64_t(ci[a]) * p.LS, p.w, p.L, p.dist);
         } else {
           cd[a] = DINF;
           ci[a] = 0xffffffffu;
@@ -608,7 +622,7 @@ __global__ void __launch_bounds__(kLT, 2) certify_large_kernel(const ReduceParam
       }
       for (uint32_t a = threadIdx.x; a < Kp; a += kLT) {
         if (a < cnt) {
-          cd[a] = exact_distance_c(y, p.bank + uint64_t(ci[a]) * p.LS, p.w, p.L, p.dist);
+          cd[a] = exact_distance_v(y, p.bank + uint64_t(ci[a]) * p.LS, p.w, p.L, p.dist);
         } else {
           cd[a] = DINF;
           ci[a] = 0xffffffffu;

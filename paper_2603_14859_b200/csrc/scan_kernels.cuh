@@ -77,7 +77,10 @@ constexpr int T = kTile;
 
 template <int LP>
 struct Shape {
-  static constexpr int R = (LP <= 48) ? 2 : 1;
+#ifndef VPET_R
+#define VPET_R 0  // voxels per lane: 0 = 2 for LP <= 48, else 1
+#endif
+  static constexpr int R = VPET_R > 0 ? VPET_R : ((LP <= 48) ? 2 : 1);
 #ifdef VPET_MINB
   static constexpr int MINB = VPET_MINB;
 #else

@@ -49,6 +49,12 @@ VARIANTS = {
     "tr3acc2": ("VPET_TREFRESH=3", "VPET_ACC2=1"),
     "npc3": ("VPET_NPC=3",),
     "npc5": ("VPET_NPC=5",),
+    "r1ch12": ("VPET_R=1", "VPET_CH=12"),
+    "r1ch16": ("VPET_R=1", "VPET_CH=16"),
+    "r1ch36": ("VPET_R=1", "VPET_CH=36"),
+    "r1ch12m12": ("VPET_R=1", "VPET_CH=12", "VPET_MINB=12"),
+    "r1nt128ch12": ("VPET_R=1", "VPET_CH=12", "VPET_NT=128"),
+    "r1nt128ch16": ("VPET_R=1", "VPET_CH=16", "VPET_NT=128"),
 }
 names = sys.argv[1:] or list(VARIANTS)
 root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2603_14859_b200", "_variants")

@@ -22,6 +22,7 @@ ap.add_argument("--save", default=None)
 ap.add_argument("--chunks", type=int, default=32, help="1 = the whole 4.44M-voxel volume (the bench workload)")
 ap.add_argument("--device-tacs", action="store_true", help="TACs resident on the device (as bench.py times)")
 ap.add_argument("--load", default=None)
+ap.add_argument("--digest", action="store_true", help="print a hash of the output maps (compare variants)")
 a = ap.parse_args()
 if a.load:
     prob = pickle.load(open(a.load, "rb"))
@@ -50,3 +51,10 @@ for s in range(a.steps):
           f"total {st['ms_total']:.2f} ms  fallback voxels {st['n_fallback']}  "
           f"launches {st['gpu_launches']}" + (f"  frame_updates {st['frame_updates']}  bound_updates {st['bound_updates']}"
                                               if a.flags & 4 else ""), flush=True)
+if a.digest:
+    import hashlib
+    h = hashlib.sha256()
+    for k in sorted(r):
+        v = r[k]
+        h.update((v.cpu().numpy() if hasattr(v, "cpu") else np.asarray(v)).tobytes())
+    print("digest", h.hexdigest()[:16], flush=True)

@@ -1,10 +1,15 @@
 #!/bin/bash
-# Time each tuning variant in paper_2603_14859_b200/_variants on the saved config-4 batch (run on the
-# GPU box); two rounds.
-python tools/profile_step.py --save /tmp/p.pkl > /dev/null
+# Time tuning variants (paper_2603_14859_b200/_variants/libvpetabc_<name>.so, or all) on the saved
+# config-4 input (run on the GPU box); two rounds.  CHUNKS=1 -> the whole 4.44M-voxel volume.
+# usage: tools/tune_run.sh [name ...]
+CH=${CHUNKS:-32}
+python tools/profile_step.py --chunks $CH --save /tmp/p.pkl > /dev/null
+libs=""
+if [ $# -gt 0 ]; then for n in "$@"; do libs="$libs paper_2603_14859_b200/_variants/libvpetabc_$n.so"; done
+else libs=$(ls paper_2603_14859_b200/_variants/libvpetabc_*.so); fi
 for round in 1 2; do
-for lib in paper_2603_14859_b200/_variants/libvpetabc_*.so; do
-  echo "== $lib"
-  VPET_LIB=$lib python tools/profile_step.py --load /tmp/p.pkl --steps 4 | tail -2 | cut -c1-60
+for lib in "" $libs; do
+  echo "== ${lib:-default}"
+  VPET_LIB=$lib python tools/profile_step.py --load /tmp/p.pkl --device-tacs --digest --steps 3 | tail -2 | cut -c1-90
 done
 done
