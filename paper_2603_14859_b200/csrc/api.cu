@@ -83,10 +83,12 @@ struct abc_ctx {
   DevBuf d_finv;  // [L] 1 / frame duration (the bank multiplies instead of dividing)
   DevBuf d_s0;    // [L] S_f(0) of the PWL grid (irreversible 2TCM draws)
   bool have_s0 = false;
+  DevBuf d_cwd;  // [L] sqrt(w_f) in FP64 (rotated scan basis)
   DevBuf d_fdur, d_fs, d_fe, d_favg, d_w, d_wsc, d_gt, d_gc, d_gframe, d_gcode, d_ft, d_fc, d_fframe;
   // work buffers
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
   DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, hbounds, tau_glob, queue;
+  DevBuf rotq, ytr, gbox;  // rotated scan basis: [L][LP] FP64 rotation, [J][LP] voxel coordinates, [2][LP] bank box
   DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp, item_log;
   DevBuf fb_tau, cl_d, cl_i, cl_cnt, fb2_list, fb2_len;  // fallback tiers (certify.cu)
   DevBuf dBt, dS2, dAt, dY2;  // ABC_FLAG_DENSE_TC operands (dense_tc.cu)
@@ -227,6 +229,11 @@ abc_status build_tables(abc_ctx* ctx) {
   CK(upload(ctx->d_favg, favg));
   CK(upload(ctx->d_w, ctx->w));
   CK(upload(ctx->d_wsc, wsc));
+  {
+    std::vector<double> cwd(L);
+    for (uint32_t f = 0; f < L; ++f) cwd[f] = ctx->unit_w ? 1.0 : std::sqrt(double(ctx->w[f]));
+    CK(upload(ctx->d_cwd, cwd));
+  }
   CK(upload(ctx->d_gt, gt));
   CK(upload(ctx->d_gc, gc));
   CK(upload(ctx->d_gframe, gfr));
@@ -327,6 +334,22 @@ ErrBound error_bound(const abc_ctx* c, uint32_t LP) {
   return e;
 }
 
+// Rotated scan basis (WL2): scan coordinates y'_k = RN32(sum_f Q_fk sqrt(w_f) y_f)
+// and s'_k likewise (FP64 sums), ||Q^T Q - I||_2 <= e_Q = kRotEps.  With a = y' - s' (reals) and
+// v = sqrt(w)(y - s), D = |v|^2:  |a - Q^T v| <= u (|y'| + |s'|) (1 + 1e-12) <= u' (2 sqrt(Y2) + sqrt(D)),
+// u' = u sqrt(1 + e_Q) (1 + 1e-12), so |A - D| <= (e_Q + 2u' + u'^2) D + (4u' + 4u'^2) sqrt(Y2 D) + 4u'^2 Y2
+// for A = |a|^2; the FP32 pass on (y', s') is the unit-weight WL2 case, |D32 - A| <= (g_L + 3u) A.
+// Combined, with margin: (g_L + 6u + e_Q) D + 4.1u sqrt(Y2 D) + 16.5u^2 Y2, doubled like the others.
+ErrBound rotated_error_bound(uint32_t LP) {
+  const double u = std::ldexp(1.0, -24);
+  const double g = LP * u / (1.0 - LP * u);
+  ErrBound e{0, 0, 0, 0};
+  e.a = 2.0 * (g + 6.1 * u + kRotEps);
+  e.b = 2.0 * 4.1 * u;
+  e.c = 2.0 * 16.5 * u * u;
+  return e;
+}
+
 // Rigorous |D' - D| bound of the dense dot form (ABC_FLAG_DENSE_TC, dense_tc.cu),
 // doubled for margin.  With a = fl(ws y), b = fl(ws s), Z = sum w (|y| + |s|)^2 <= 4 Y2 + 4 sqrt(Y2 D) + D:
 //   prescaling        |sum (a-b)^2 - D| <= (2u + u^2) D + 2u sqrt(D Z) + u^2 Z
@@ -351,7 +374,7 @@ ErrBound dense_error_bound(uint32_t L) {
 
 namespace vpet {
 cudaError_t ensure_smem_attr(const void* func, size_t bytes) {
-  if (bytes <= 48 * 1024) return cudaSuccess;
+  if (bytes <= 32 * 1024) return cudaSuccess;  // + static shared memory stays under the 48 KB default
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -363,7 +386,14 @@ cudaError_t ensure_smem_attr(const void* func, size_t bytes) {
   int optin = 0;
   e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return e;
-  if (bytes > size_t(optin)) return cudaErrorInvalidValue;
+  cudaFuncAttributes fa{};
+  e = cudaFuncGetAttributes(&fa, func);
+  if (e != cudaSuccess) return e;
+  if (bytes + fa.sharedSizeBytes <= 48 * 1024) {
+    have = bytes;
+    return cudaSuccess;
+  }
+  if (bytes + fa.sharedSizeBytes > size_t(optin)) return cudaErrorInvalidValue;
   e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
   if (e == cudaSuccess) have = bytes;
   return e;
@@ -617,6 +647,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (dense) need += dense_bank_bytes(N) + dense_voxel_bytes(J) + 4 * J;
   const bool tree = !exact && !dense && !(ctx->cfg.flags & ABC_FLAG_NO_TREE) && N < (1ull << 31);
   const uint64_t ntile = (N + kTile - 1) / kTile, nsuper = (ntile + kSuper - 1) / kSuper;
+  // rotated scan basis: WL2, tree mode, frame reordering allowed, LP <= 64
+  static const bool rot_env = getenv("VPET_ROT") ? atoi(getenv("VPET_ROT")) != 0 : true;  // tuning knob
+  const bool rotated = rot_env && tree && ctx->dist_wl2() && !(ctx->cfg.flags & ABC_FLAG_NO_REORDER) && LP <= 64;
   const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
   // draw-range split of the tree scan (interleaved super-tiles): balances heavy voxels over SMs
   uint32_t nparts = 1;
@@ -651,6 +684,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   const size_t vsort_tmp = tree ? voxel_sort_temp_bytes(J) : 0;
   if (tree) need += N * (8 + 8 + 4 + 4 + 4 + 4 * kNPC) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper + nhyper);
   if (tree) need += 24 * J + vsort_tmp;
+  if (rotated) need += sizeof(double) * L * LP + sizeof(float) * J * LP;
   if (!eps) need += (size_t(8) * heap_stride(std::max<uint32_t>(K, 1)) + 4) * J * nparts + 4 * J;  // heaps
   need += size_t(12) * J * (n ? n : 1);                  // exact heaps (last-resort fallback)
   // fallback collector lists: cl_cap (the certification capacity) entries for up to cl_voxels voxels
@@ -706,6 +740,11 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(ctx->hbounds.ensure(sizeof(float) * 2 * LP * nhyper));
     CK(ctx->tau_glob.ensure(4 * J));
     CK(ctx->queue.ensure(16));
+    if (rotated) {
+      CK(ctx->rotq.ensure(sizeof(double) * L * LP));
+      CK(ctx->ytr.ensure(sizeof(float) * J * LP));
+      CK(ctx->gbox.ensure(sizeof(float) * 2 * LP));
+    }
     CK(ctx->vkeys.ensure(8 * J));
     CK(ctx->vkeys_alt.ensure(8 * J));
     CK(ctx->vvals.ensure(4 * J));
@@ -809,7 +848,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   ctx->bank_L = L;
   rec(EV_BANK);
 
-  const ErrBound eb = dense ? dense_error_bound(L) : error_bound(ctx, LP);
+  const ErrBound eb = dense ? dense_error_bound(L) : (rotated ? rotated_error_bound(LP) : error_bound(ctx, LP));
   if (!exact && !dense) {
     OrderParams op{};
     op.bank = ctx->bank.as<float>();
@@ -842,6 +881,11 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       op.hbounds = ctx->hbounds.as<float>();
       op.hs = hs;
       op.nhyper = nhyper;
+      if (rotated) {
+        op.rotq = ctx->rotq.as<double>();
+        op.cw = ctx->d_cwd.as<double>();
+        op.gbox = ctx->gbox.as<float>();
+      }
     }
     CK(launch_order(op, st, &launches));
     if (tree) {
@@ -863,6 +907,10 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       vp.sort_temp = ctx->vsort_temp.p;
       vp.sort_temp_bytes = vsort_tmp;
       CK(launch_voxel_order(vp, st, &launches));
+      if (rotated) {
+        CK(launch_voxel_rotate(d_tacs, J, L, LP, ctx->rotq.as<double>(), ctx->ytr.as<float>(), st));
+        ++launches;
+      }
     }
   }
   CK(join_tacs());
@@ -923,6 +971,8 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       sp.tau_glob = eps ? nullptr : ctx->tau_glob.as<unsigned int>();
       sp.queue = ctx->queue.as<unsigned int>();
       sp.vorder = ctx->vorder.as<uint32_t>();
+      sp.ytr = rotated ? ctx->ytr.as<float>() : nullptr;
+      sp.gbox = rotated ? ctx->gbox.as<float>() : nullptr;
       if (!eps) launch_fill_u32(ctx->tau_glob.as<uint32_t>(), 0x7f800000u, J, st);
       CK(cudaMemsetAsync(ctx->queue.p, 0, 16, st));
       launches += eps ? 0 : 1;
@@ -1356,13 +1406,13 @@ void abc_destroy(abc_ctx* ctx) {
   cudaSetDevice(ctx->dev);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs2[] = {&ctx->fmean, &ctx->cov, &ctx->pcs, &ctx->pminmax, &ctx->keys, &ctx->keys_alt, &ctx->vals,
-                     &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob,
+                     &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob, &ctx->rotq, &ctx->ytr, &ctx->gbox,
                      &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp, &ctx->item_log,
                      &ctx->dBt, &ctx->dS2, &ctx->dAt, &ctx->dY2,
                      &ctx->env_idx, &ctx->env_t, &ctx->env_q, &ctx->proj, &ctx->pat_ab,
                      &ctx->fb_tau, &ctx->cl_d, &ctx->cl_i, &ctx->cl_cnt, &ctx->fb2_list, &ctx->fb2_len};
   for (DevBuf* b : bufs2) b->release();
-  DevBuf* bufs[] = {&ctx->d_finv, &ctx->d_s0, &ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc,
+  DevBuf* bufs[] = {&ctx->d_finv, &ctx->d_s0, &ctx->d_prior, &ctx->d_fdur, &ctx->d_fs,  &ctx->d_fe,   &ctx->d_favg, &ctx->d_w,        &ctx->d_wsc, &ctx->d_cwd,
                     &ctx->d_gt,   &ctx->d_gc,  &ctx->d_gframe, &ctx->d_gcode, &ctx->d_ft, &ctx->d_fc,       &ctx->d_fframe,
                     &ctx->bank,   &ctx->bankp, &ctx->var,    &ctx->perm,   &ctx->wsp,        &ctx->heap,
                     &ctx->heap_cnt, &ctx->tacs, &ctx->fb_list, &ctx->fb_len, &ctx->work,     &ctx->hd,

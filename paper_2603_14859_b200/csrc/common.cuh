@@ -233,8 +233,17 @@ struct OrderParams {
   float* hbounds;     // [nhyper][2][LP] (hyper-tile = hs consecutive super-tiles)
   uint32_t hs;
   uint64_t nhyper;
+  // rotated scan basis (WL2, tree mode): rotq != nullptr selects it
+  double* rotq;         // [L][LP] out: rotq[f][k] = Q[a][k] sqrt(w_f), f = perm[a]; scan coordinate k = sum_f rotq[f][k] x_f
+  const double* cw;     // [L] sqrt(w_f) in FP64 (1 for unit weights)
+  float* gbox;          // [2][LP] out (rotated basis): min / max of bankp over all draws
 };
 cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launches);
+// Rotated voxel coordinates ytr[j][k] = RN32(sum_f rotq[f][k] y_f) (FP64 sums), k < LP.
+cudaError_t launch_voxel_rotate(const float* tacs, uint64_t J, uint32_t L, uint32_t LP, const double* rotq, float* ytr,
+                                cudaStream_t st);
+// ||Q^T Q - I||_2 assumed by the rotated-basis error bound (checked on device; Q = I otherwise)
+constexpr double kRotEps = 1e-10;
 size_t order_sort_temp_bytes(uint64_t N);
 
 // Voxel order for the tree scan: voxels sorted by the projection of their prescaled TAC on the
@@ -311,6 +320,8 @@ struct ScanParams {
   unsigned long long* item_log;  // diagnostics (env VPET_ITEMLOG): [item][4] = start ns, end ns, SM, voxel tile
   const uint32_t* vorder;   // [J] voxel processed in slot j (tree mode) or nullptr (identity)
   const int* bad;           // set by the finite check when a TAC value is not finite: skip all work
+  const float* ytr;         // [J][LP] rotated voxel coordinates (rotated basis) or nullptr (frame basis)
+  const float* gbox;        // [2][LP] rotated basis: min / max over the whole scan bank (tail bounds)
 };
 // Candidate heaps: 8-ary max-heaps; node i lives at slot i + kHeapOff of a (voxel, part) row of
 // heap_stride(K) keys, so the 8 children of node i (slots 8i + 8 .. 8i + 15) are one 64-B group.

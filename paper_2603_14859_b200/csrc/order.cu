@@ -170,6 +170,133 @@ __global__ void __launch_bounds__(32) pca_kernel(const OrderParams p) {
   }
 }
 
+// ---- rotated scan basis (WL2, tree mode, LP <= kRotMaxLP): eigenvectors of the covariance of
+// the prescaled bank by cyclic Jacobi (round-robin parallel ordering: LP / 2 disjoint rotations
+// per round), one block; columns in descending eigenvalue order.  Out: rotq[f][k] = Q[a][k] * cw[f]
+// for the real frames f = perm[a].  The bank's curves span few directions (2TCM: ~4 carry all
+// the variance), so in this basis a tile's box is thin in every coordinate.
+// Exactness does not rest on Q being eigenvectors, only on its orthogonality, which is checked:
+// LP * max|Q^T Q - I| > kRotEps falls back to Q = I. ----
+constexpr uint32_t kRotMaxLP = 64;
+__global__ void __launch_bounds__(256) rot_kernel(const OrderParams p) {
+  extern __shared__ double rsm[];
+  const uint32_t n = p.LP;  // a multiple of 4
+  double* A = rsm;          // [n][n]
+  double* V = rsm + n * n;  // [n][n]
+  __shared__ double cs_c[kRotMaxLP / 2], cs_s[kRotMaxLP / 2];
+  __shared__ int pp[kRotMaxLP / 2], pq[kRotMaxLP / 2];
+  __shared__ double red[2][8];
+  __shared__ int rank[kRotMaxLP];
+  __shared__ int stop;
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  for (uint32_t e = tid; e < n * n; e += nt) {
+    A[e] = p.cov[e];
+    V[e] = (e / n == e % n) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  auto block_sum2 = [&](double x, double y, double& sx, double& sy) {
+    for (int o = 16; o > 0; o >>= 1) {
+      x += __shfl_xor_sync(0xffffffffu, x, o);
+      y += __shfl_xor_sync(0xffffffffu, y, o);
+    }
+    if ((tid & 31) == 0) {
+      red[0][tid >> 5] = x;
+      red[1][tid >> 5] = y;
+    }
+    __syncthreads();
+    sx = 0.0;
+    sy = 0.0;
+    for (uint32_t w = 0; w < nt / 32; ++w) {
+      sx += red[0][w];
+      sy += red[1][w];
+    }
+    __syncthreads();
+  };
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double off = 0.0, dia = 0.0;
+    for (uint32_t e = tid; e < n * n; e += nt) {
+      const double a = A[e];
+      if (e / n == e % n) dia += a * a;
+      else off += a * a;
+    }
+    block_sum2(off, dia, off, dia);
+    if (off <= 1e-30 * dia || off == 0.0) break;
+    for (uint32_t r = 0; r + 1 < n; ++r) {
+      if (tid < n / 2) {
+        // round-robin: position 0 holds index 0, position i >= 1 holds ((i - 1 + r) mod (n - 1)) + 1
+        auto at = [&](uint32_t pos) { return pos == 0 ? 0u : ((pos - 1 + r) % (n - 1)) + 1; };
+        uint32_t a = at(tid), b = at(n - 1 - tid);
+        if (a > b) { const uint32_t t = a; a = b; b = t; }
+        const double apq = A[a * n + b];
+        double c = 1.0, sn = 0.0;
+        if (fabs(apq) > 1e-300) {
+          const double th = (A[b * n + b] - A[a * n + a]) / (2.0 * apq);
+          const double t = fabs(th) > 1e150 ? 0.5 / th : copysign(1.0, th) / (fabs(th) + sqrt(th * th + 1.0));
+          c = 1.0 / sqrt(t * t + 1.0);
+          sn = t * c;
+        }
+        cs_c[tid] = c;
+        cs_s[tid] = sn;
+        pp[tid] = int(a);
+        pq[tid] = int(b);
+      }
+      __syncthreads();
+      for (uint32_t e = tid; e < (n / 2) * n; e += nt) {  // columns of A and V
+        const uint32_t k = e / n, i = e % n;
+        const uint32_t a = uint32_t(pp[k]), b = uint32_t(pq[k]);
+        const double c = cs_c[k], sn = cs_s[k];
+        const double x = A[i * n + a], y = A[i * n + b];
+        A[i * n + a] = c * x - sn * y;
+        A[i * n + b] = sn * x + c * y;
+        const double u = V[i * n + a], v = V[i * n + b];
+        V[i * n + a] = c * u - sn * v;
+        V[i * n + b] = sn * u + c * v;
+      }
+      __syncthreads();
+      for (uint32_t e = tid; e < (n / 2) * n; e += nt) {  // rows of A
+        const uint32_t k = e / n, j = e % n;
+        const uint32_t a = uint32_t(pp[k]), b = uint32_t(pq[k]);
+        const double c = cs_c[k], sn = cs_s[k];
+        const double x = A[a * n + j], y = A[b * n + j];
+        A[a * n + j] = c * x - sn * y;
+        A[b * n + j] = sn * x + c * y;
+      }
+      __syncthreads();
+    }
+  }
+  // descending eigenvalue order (stable)
+  if (tid < n) {
+    const double lk = A[tid * n + tid];
+    int rk = 0;
+    for (uint32_t j = 0; j < n; ++j) {
+      const double lj = A[j * n + j];
+      rk += (lj > lk || (lj == lk && j < tid)) ? 1 : 0;
+    }
+    rank[tid] = rk;
+  }
+  if (tid == 0) stop = 0;
+  __syncthreads();
+  // orthogonality defect of V (columns permute without changing it)
+  double md = 0.0;
+  for (uint32_t e = tid; e < n * n; e += nt) {
+    const uint32_t i = e / n, j = e % n;
+    double d = 0.0;
+    for (uint32_t a = 0; a < n; ++a) d = fma(V[a * n + i], V[a * n + j], d);
+    md = fmax(md, fabs(d - (i == j ? 1.0 : 0.0)));
+  }
+  for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+  if ((tid & 31) == 0 && double(n) * md + 1e-14 > kRotEps) atomicExch(&stop, 1);
+  __syncthreads();
+  // a failed check (never seen) falls back to Q = I: exactly orthogonal, the frame basis
+  const bool ok = stop == 0;
+  for (uint32_t e = tid; e < p.L * n; e += nt) {
+    const uint32_t a = e / n, k = e % n;  // scan position a (a real frame: a < L), eigen-column k
+    const int f = p.perm[a];
+    const double q = ok ? V[a * n + k] : (a == k ? 1.0 : 0.0);
+    if (f >= 0) p.rotq[uint32_t(f) * n + (ok ? uint32_t(rank[k]) : k)] = q * p.cw[f];
+  }
+}
+
 __device__ __forceinline__ unsigned int f2ord(float x) {
   unsigned int u = __float_as_uint(x);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
@@ -363,7 +490,7 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
 // coalesced 16-B loads into shared memory, then written out frame-contiguous. ----
 constexpr int kPermWarps = 4;
 __global__ void __launch_bounds__(32 * kPermWarps) permute_kernel(const OrderParams p) {
-  extern __shared__ float psm[];  // [kPermWarps][kTile][LS + 1]
+  extern __shared__ double psm_d[];  // rotated basis: [L][LP] rotq; then [kPermWarps][kTile][max(LS, LP) + 1] floats
   __shared__ int sperm[kMaxLP];
   __shared__ float swsp[kMaxLP];
   __shared__ uint32_t sidx[kPermWarps][kTile];
@@ -371,10 +498,14 @@ __global__ void __launch_bounds__(32 * kPermWarps) permute_kernel(const OrderPar
     sperm[k] = p.perm[k];
     swsp[k] = p.wsp[k];
   }
+  const double* srot = psm_d;
+  if (p.rotq)
+    for (uint32_t e = threadIdx.x; e < p.L * p.LP; e += blockDim.x) psm_d[e] = p.rotq[e];
+  float* psm = reinterpret_cast<float*>(psm_d + (p.rotq ? p.L * p.LP : 0));
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t LS = p.LS, Q = LS / 4, stride = LS + 1;
-  float* rows = psm + size_t(wid) * kTile * stride;
+  const uint32_t LS = p.LS, Q = LS / 4, stride = (LS > p.LP ? LS : p.LP) + 1;
+  float* rows = psm + size_t(wid) * kTile * stride * (p.rotq ? 2 : 1);
   const uint64_t ntile = (p.N + kTile - 1) / kTile;
   for (uint64_t t = uint64_t(blockIdx.x) * kPermWarps + wid; t < ntile; t += uint64_t(gridDim.x) * kPermWarps) {
     const uint64_t j0 = t * kTile;
@@ -405,10 +536,48 @@ __global__ void __launch_bounds__(32 * kPermWarps) permute_kernel(const OrderPar
       }
     }
     __syncwarp();
-    // the tile's nr x LP block of bankp is contiguous (LP % 4 == 0): 16-B stores, lane q writes
-    // frames 4(q % QP) .. +3 of row q / QP
     const uint32_t QP = p.LP / 4;
     float4* dst = reinterpret_cast<float4*>(p.bankp + j0 * p.LP);
+    if (p.rotq) {
+      // rotated basis: lane r computes row r's LP coordinates, RN32 of FP64 sums over the frames,
+      // into its own row of rows (overwritten in place after the whole row is read), negated
+      float* orows = rows + kTile * stride;  // [kTile][stride] rotated rows of this warp
+      if (uint32_t(lane) < nr) {
+        const float* row = rows + lane * stride;
+        float* orow = orows + lane * stride;
+        for (uint32_t k0 = 0; k0 < p.LP; k0 += 4) {
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          for (uint32_t f = 0; f < p.L; ++f) {
+            const double x = double(row[f]);
+            const double* q = srot + f * p.LP + k0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(q[u], x, acc[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) orow[k0 + u] = -__double2float_rn(acc[u]);
+        }
+      }
+      __syncwarp();
+      for (uint32_t q = lane; q < nr * QP; q += 32) {
+        const float* row = orows + (q / QP) * stride + 4 * (q % QP);
+        dst[q] = make_float4(row[0], row[1], row[2], row[3]);
+      }
+      if (p.tree && p.tbounds)
+        for (uint32_t k = lane; k < p.LP; k += 32) {
+          float lo = 3.0e38f, hi = -3.0e38f;
+          for (uint32_t r = 0; r < nr; ++r) {
+            const float v = orows[r * stride + k];
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+          }
+          p.tbounds[(t * 2 + 0) * p.LP + k] = lo;
+          p.tbounds[(t * 2 + 1) * p.LP + k] = hi;
+        }
+      __syncwarp();
+      continue;
+    }
+    // the tile's nr x LP block of bankp is contiguous (LP % 4 == 0): 16-B stores, lane q writes
+    // frames 4(q % QP) .. +3 of row q / QP
     for (uint32_t q = lane; q < nr * QP; q += 32) {
       const float* row = rows + (q / QP) * stride;
       const uint32_t k = 4 * (q % QP);
@@ -464,6 +633,19 @@ __global__ void __launch_bounds__(128) hyper_bounds_kernel(const OrderParams p, 
     }
     p.hbounds[(h * 2 + 0) * p.LP + k] = lo;
     p.hbounds[(h * 2 + 1) * p.LP + k] = hi;
+  }
+}
+
+// whole-bank box of the scan coordinates (rotated basis: the tail bound of each voxel), one block
+__global__ void __launch_bounds__(128) global_box_kernel(const OrderParams p) {
+  for (uint32_t k = threadIdx.x; k < p.LP; k += blockDim.x) {
+    float lo = 3.0e38f, hi = -3.0e38f;
+    for (uint64_t h = 0; h < p.nhyper; ++h) {
+      lo = fminf(lo, p.hbounds[(h * 2 + 0) * p.LP + k]);
+      hi = fmaxf(hi, p.hbounds[(h * 2 + 1) * p.LP + k]);
+    }
+    p.gbox[k] = lo;
+    p.gbox[p.LP + k] = hi;
   }
 }
 
@@ -542,7 +724,40 @@ __global__ void __launch_bounds__(256) voxel_key_kernel(const VoxelOrderParams p
   }
 }
 
+// ---- rotated voxel coordinates: thread per voxel, ytr[j][k] = RN32(sum_f rotq[f][k] y_f) ----
+__global__ void __launch_bounds__(128) voxel_rotate_kernel(const float* __restrict__ tacs, uint64_t J, uint32_t L,
+                                                           uint32_t LP, const double* __restrict__ rotq,
+                                                           float* __restrict__ ytr) {
+  extern __shared__ double vq[];  // [L][LP]
+  for (uint32_t e = threadIdx.x; e < L * LP; e += blockDim.x) vq[e] = rotq[e];
+  __syncthreads();
+  for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < J; j += uint64_t(gridDim.x) * blockDim.x) {
+    const float* y = tacs + j * L;
+    float4* out = reinterpret_cast<float4*>(ytr + j * LP);
+    for (uint32_t k0 = 0; k0 < LP; k0 += 4) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (uint32_t f = 0; f < L; ++f) {
+        const double x = double(__ldg(y + f));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = fma(vq[f * LP + k0 + u], x, acc[u]);
+      }
+      out[k0 / 4] = make_float4(__double2float_rn(acc[0]), __double2float_rn(acc[1]), __double2float_rn(acc[2]),
+                                __double2float_rn(acc[3]));
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_voxel_rotate(const float* tacs, uint64_t J, uint32_t L, uint32_t LP, const double* rotq, float* ytr,
+                                cudaStream_t st) {
+  if (LP > kRotMaxLP) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(double) * L * LP;
+  cudaError_t e = ensure_smem_attr((const void*)voxel_rotate_kernel, smem);
+  if (e != cudaSuccess) return e;
+  voxel_rotate_kernel<<<148 * 8, 128, smem, st>>>(tacs, J, L, LP, rotq, ytr);
+  return cudaGetLastError();
+}
 
 size_t voxel_sort_temp_bytes(uint64_t J) { return radix_temp_bytes(J); }
 
@@ -569,6 +784,14 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
     proj_minmax_kernel<<<148 * 4, 256, 0, st>>>(p);
     key_kernel<<<148 * 8, 256, 0, st>>>(p);
     *launches += 4;
+    if (p.rotq) {
+      if (p.LP > kRotMaxLP) return cudaErrorInvalidValue;
+      const size_t rs = sizeof(double) * 2 * p.LP * p.LP;
+      cudaError_t er = ensure_smem_attr((const void*)rot_kernel, rs);
+      if (er != cudaSuccess) return er;
+      rot_kernel<<<1, 256, rs, st>>>(p);
+      *launches += 1;
+    }
     // the lowest 8 key bits (the two finest levels of the curve) are not sorted: one radix pass
     // less, same scan time (Morton, measured: 0 / 8 / 16 bits -> scan 19.6 / 19.5 / 20.3 ms; with
     // the Hilbert order 24 unsorted bits double the scan); the order is free.
@@ -581,7 +804,9 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
     q.order = nullptr;
   }
   {
-    const size_t psmem = sizeof(float) * kPermWarps * kTile * (p.LS + 1);
+    if (!p.tree) q.rotq = nullptr;
+    const size_t psmem = sizeof(float) * kPermWarps * kTile * ((p.LS > p.LP ? p.LS : p.LP) + 1) * (q.rotq ? 2 : 1) +
+                         (q.rotq ? sizeof(double) * p.L * p.LP : 0);
     cudaError_t ea = ensure_smem_attr((const void*)permute_kernel, psmem);
     if (ea != cudaSuccess) return ea;
     permute_kernel<<<148 * 8, 32 * kPermWarps, psmem, st>>>(q);
@@ -593,6 +818,10 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
     super_bounds_kernel<<<unsigned(nsup), 128, 0, st>>>(p, ntile);
     hyper_bounds_kernel<<<unsigned(p.nhyper), 128, 0, st>>>(p, nsup);
     *launches += 2;
+    if (p.rotq && p.gbox) {
+      global_box_kernel<<<1, 128, 0, st>>>(p);
+      *launches += 1;
+    }
   }
   return cudaGetLastError();
 }

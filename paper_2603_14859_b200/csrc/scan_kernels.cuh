@@ -68,6 +68,10 @@ constexpr int T = kTile;
 #ifndef VPET_RREFRESH
 #define VPET_RREFRESH 0  // and every VPET_RREFRESH rows inside a tile (0: off)
 #endif
+#ifndef VPET_HEAD
+#define VPET_HEAD 8  // rotated basis: coordinates evaluated before a row's first test (multiple of 4)
+#endif
+constexpr int kHead = VPET_HEAD;
 #ifndef VPET_SHEAP
 #define VPET_SHEAP 0  // keep the top of each candidate heap in shared memory (tree scan)
 #endif
@@ -296,9 +300,10 @@ struct Voxels {
   float taup[R];  // own (part) heap root, +inf until the heap is full
   uint32_t cnt[R];
   uint32_t vox[R];  // voxel index (>= J for an empty slot)
+  float rv[R];      // rotated basis: lower bound on the coordinates >= kHead of every draw's D32 terms
 };
 
-template <int LP, int R>
+template <int LP, int R, bool ROT = false>
 __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& V, int tid, uint64_t vtile) {
   const float INF = __int_as_float(0x7f800000);
 #pragma unroll
@@ -314,12 +319,38 @@ __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& 
     uint64_t v = (valid && p.vorder) ? uint64_t(__ldg(p.vorder + slot)) : slot;
     V.vox[r] = uint32_t(v);
     const float* yr = p.tacs + (valid ? v : 0) * p.L;
+    if (p.ytr) {  // rotated basis: the voxel's scan coordinates were computed by voxel_rotate_kernel
+      const float4* yt = reinterpret_cast<const float4*>(p.ytr + (valid ? v : 0) * uint64_t(LP));
 #pragma unroll
-    for (int k = 0; k < LP; k += 2) {
-      int s0 = __ldg(p.perm + k), s1 = __ldg(p.perm + k + 1);
-      float a = (valid && s0 >= 0) ? __fmul_rn(__ldg(p.wsp + k), __ldg(yr + s0)) : 0.0f;
-      float b = (valid && s1 >= 0) ? __fmul_rn(__ldg(p.wsp + k + 1), __ldg(yr + s1)) : 0.0f;
-      V.y[r][k / 2] = make_float2(a, b);
+      for (int k = 0; k < LP; k += 4) {
+        const float4 q = valid ? __ldg(yt + k / 4) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        V.y[r][k / 2] = make_float2(q.x, q.y);
+        V.y[r][k / 2 + 1] = make_float2(q.z, q.w);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < LP; k += 2) {
+        int s0 = __ldg(p.perm + k), s1 = __ldg(p.perm + k + 1);
+        float a = (valid && s0 >= 0) ? __fmul_rn(__ldg(p.wsp + k), __ldg(yr + s0)) : 0.0f;
+        float b = (valid && s1 >= 0) ? __fmul_rn(__ldg(p.wsp + k + 1), __ldg(yr + s1)) : 0.0f;
+        V.y[r][k / 2] = make_float2(a, b);
+      }
+    }
+    V.rv[r] = 0.0f;
+    if (ROT && valid) {
+      // sum over the tail coordinates of the squared gap to the whole bank's box, the same FP32
+      // gap as bound_chunk (so every row's term is >= it), squares and sum in FP64, rounded down
+      double t = 0.0;
+#pragma unroll
+      for (int k = kHead; k < LP; k += 2) {
+        const float2 yk = V.y[r][k / 2];
+        const float lo0 = __ldg(p.gbox + k), hi0 = __ldg(p.gbox + LP + k);
+        const float lo1 = __ldg(p.gbox + k + 1), hi1 = __ldg(p.gbox + LP + k + 1);
+        const float g0 = fmaxf(fmaxf(__fadd_rn(yk.x, lo0), -__fadd_rn(yk.x, hi0)), 0.0f);
+        const float g1 = fmaxf(fmaxf(__fadd_rn(yk.y, lo1), -__fadd_rn(yk.y, hi1)), 0.0f);
+        t += double(g0) * double(g0) + double(g1) * double(g1);
+      }
+      V.rv[r] = __double2float_rd(t * (1.0 - 1e-14));
     }
     V.cnt[r] = 0;
     V.taup[r] = INF;
@@ -525,6 +556,47 @@ __device__ __forceinline__ void eval_row(const ScanParams& p, Voxels<LP, R>& V, 
   bool go = Chunks<LP, R, DIST, false, 0>::run(V, sr, sr, acc, w, !p.prune);
   if (COUNT && !VPET_COUNT_PUSH) work += w;
   if (go) finish_row<LP, R, COUNT, SH>(p, V, acc, i, part, work, htop_s);
+}
+
+// Coordinates [Q0, Q1) of the distance of R voxels to one bank row (scan order).
+template <int LP, int R, int DIST, int Q0, int Q1, class Src>
+__device__ __forceinline__ void dist_range(const Voxels<LP, R>& V, const Src sr, Acc (&acc)[R]) {
+#pragma unroll
+  for (int q = Q0; q < Q1; q += 4) {
+    const float4 s4 = sr.ld(q);
+    const float2 sa = make_float2(s4.x, s4.y);
+    const float2 sc = make_float2(s4.z, s4.w);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float2 d0 = __fadd2_rn(V.y[r][q / 2], sa);
+      float2 d1 = __fadd2_rn(V.y[r][q / 2 + 1], sc);
+      acc[r].a = __ffma2_rn(d0, d0, acc[r].a);
+      acc_second(acc[r]) = __ffma2_rn(d1, d1, acc_second(acc[r]));
+    }
+  }
+}
+
+// Rotated basis (WL2): the first kHead coordinates, then a warp test with the voxel's tail bound
+// rv: a row is dropped when fl(prefix + rv) >= tau_hi = tau (1 + 2 (LP + kHead + 4) u) (rounded up),
+// which implies D32 >= tau (the prefix is a FP32 sum of m + 1 terms, the rest of D32
+// adds terms >= the gaps summed in rv, and the whole sum rounds by at most gamma_{LP+1}).
+template <int LP, int R, int DIST, bool COUNT, bool SH = false>
+__device__ __forceinline__ void eval_row_rot(const ScanParams& p, Voxels<LP, R>& V, const SmemSrc sr, uint64_t i,
+                                             uint32_t part, unsigned long long& work, uint32_t htop_s = 0) {
+  constexpr float kTauHi = 1.0f + float(2 * (LP + kHead + 4)) * 5.9604644775390625e-8f;  // exact: LP + kHead + 4 < 2^22
+  Acc acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc_zero(acc[r]);
+  dist_range<LP, R, DIST, 0, kHead>(V, sr, acc);
+  bool alive = !p.prune;
+#pragma unroll
+  for (int r = 0; r < R; ++r) alive |= __fadd_rn(acc_total(acc[r]), V.rv[r]) < __fmul_ru(V.tau[r], kTauHi);
+  const bool go = __any_sync(0xffffffffu, alive);
+  if (COUNT && !VPET_COUNT_PUSH) work += uint64_t(kHead) * R;
+  if (!go) return;
+  dist_range<LP, R, DIST, kHead, LP>(V, sr, acc);
+  if (COUNT && !VPET_COUNT_PUSH) work += uint64_t(LP - kHead) * R;
+  finish_row<LP, R, COUNT, SH>(p, V, acc, i, part, work, htop_s);
 }
 
 // Two rows at once: their first chunks run interleaved (twice the independent FMA chains, one
@@ -792,7 +864,7 @@ __device__ __forceinline__ float mean_lb(const float* yb, const float* lo) {
 // =============================================================================================
 // Tree scan: Morton-ordered bank, hyper-tile / super-tile / tile bounds, best-first order.
 // =============================================================================================
-template <int LP, int DIST, bool COUNT>
+template <int LP, int DIST, bool COUNT, bool ROT = false>
 __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const ScanParams p) {
   constexpr int R = Shape<LP>::R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -886,7 +958,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
     if (p.item_log && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_item0));
     const uint64_t nsub = (p.nhyper > part) ? (p.nhyper - part + S - 1) / S : 0;  // hyper-tiles of this part
     Voxels<LP, R> V;
-    load_voxels<LP, R>(p, V, tid, vt);
+    load_voxels<LP, R, ROT>(p, V, tid, vt);
 
     // ---- best-first order of this part's hyper-tiles: key = min over warps of the lower bound of
     // the warp's mean TAC against the hyper-tile box (a heuristic order; exactness does not depend
@@ -1054,7 +1126,10 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
             refresh_issue<LP, R>(p, V, gnow4);
             const uint32_t d0 = nd < kTrefreshRows ? nd : kTrefreshRows;
             for (; d < d0; ++d)
-              eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
+              {
+              if constexpr (ROT) eval_row_rot<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
+              else eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
+            }
             refresh_apply<LP, R>(V, gnow4);
           }
           if (VPET_PAIR)
@@ -1063,7 +1138,10 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
                                                               SmemSrc{sb_a + 4u * (d + 1) * LP}, si[d + 1],
                                                               part, work, htop_s);
           for (; d < nd; ++d)
-            eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
+            {
+              if constexpr (ROT) eval_row_rot<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
+              else eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
+            }
         }
         __syncwarp();
         if (lane == 0) {
@@ -1099,10 +1177,10 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
   finish_counts(p, work, bwork, lane, COUNT);
 }
 
-template <int LP, int DIST, bool COUNT, bool TREE>
+template <int LP, int DIST, bool COUNT, bool TREE, bool ROT = false>
 cudaError_t launch_one(const ScanParams& p, cudaStream_t st) {
   using S = Shape<LP>;
-  auto kern = TREE ? scan_tree_kernel<LP, DIST, COUNT> : scan_flat_kernel<LP, DIST, COUNT>;
+  auto kern = TREE ? scan_tree_kernel<LP, DIST, COUNT, ROT> : scan_flat_kernel<LP, DIST, COUNT>;
   {
     cudaError_t e = ensure_smem_attr((const void*)kern, S::SMEM);
     if (e != cudaSuccess) return e;
@@ -1128,8 +1206,14 @@ cudaError_t launch_one(const ScanParams& p, cudaStream_t st) {
 
 template <int DIST>
 cudaError_t launch_dist(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st) {
+  // rotated basis (p.ytr): WL2, kHead < LP <= 64 (api.cu selects it only there)
+  const bool rot = p.ytr != nullptr;
 #define X(v)                                                                          \
   if (LP == v) {                                                                      \
+    if constexpr (DIST == ABC_DIST_WL2 && v > kHead && v <= 64) {                     \
+      if (tree && rot)                                                                \
+        return count_work ? launch_one<v, DIST, true, true, true>(p, st) : launch_one<v, DIST, false, true, true>(p, st); \
+    }                                                                                 \
     if (tree) return count_work ? launch_one<v, DIST, true, true>(p, st) : launch_one<v, DIST, false, true>(p, st); \
     return count_work ? launch_one<v, DIST, true, false>(p, st) : launch_one<v, DIST, false, false>(p, st);         \
   }

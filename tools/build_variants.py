@@ -49,6 +49,7 @@ VARIANTS = {
     "tr3acc2": ("VPET_TREFRESH=3", "VPET_ACC2=1"),
     "npc3": ("VPET_NPC=3",),
     "npc5": ("VPET_NPC=5",),
+    "quota0": ("VPET_QUOTA=0",),
     "r1ch12": ("VPET_R=1", "VPET_CH=12"),
     "r1ch16": ("VPET_R=1", "VPET_CH=16"),
     "r1ch36": ("VPET_R=1", "VPET_CH=36"),
