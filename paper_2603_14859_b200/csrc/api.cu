@@ -647,9 +647,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (dense) need += dense_bank_bytes(N) + dense_voxel_bytes(J) + 4 * J;
   const bool tree = !exact && !dense && !(ctx->cfg.flags & ABC_FLAG_NO_TREE) && N < (1ull << 31);
   const uint64_t ntile = (N + kTile - 1) / kTile, nsuper = (ntile + kSuper - 1) / kSuper;
-  // rotated scan basis: WL2, tree mode, frame reordering allowed, LP <= 64
+  // rotated scan basis: WL2, tree mode, frame reordering allowed
   static const bool rot_env = getenv("VPET_ROT") ? atoi(getenv("VPET_ROT")) != 0 : true;  // tuning knob
-  const bool rotated = rot_env && tree && ctx->dist_wl2() && !(ctx->cfg.flags & ABC_FLAG_NO_REORDER) && LP <= 64;
+  const bool rotated = rot_env && tree && ctx->dist_wl2() && !(ctx->cfg.flags & ABC_FLAG_NO_REORDER);
   const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
   // draw-range split of the tree scan (interleaved super-tiles): balances heavy voxels over SMs
   uint32_t nparts = 1;

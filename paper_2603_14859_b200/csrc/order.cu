@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(32) pca_kernel(const OrderParams p) {
 // the variance), so in this basis a tile's box is thin in every coordinate.
 // Exactness does not rest on Q being eigenvectors, only on its orthogonality, which is checked:
 // LP * max|Q^T Q - I| > kRotEps falls back to Q = I. ----
-constexpr uint32_t kRotMaxLP = 64;
+constexpr uint32_t kRotMaxLP = kMaxLP;
 __global__ void __launch_bounds__(256) rot_kernel(const OrderParams p) {
   extern __shared__ double rsm[];
   const uint32_t n = p.LP;  // a multiple of 4
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(32 * kPermWarps) permute_kernel(const OrderPar
       myi = p.order ? p.order[j0 + lane] : uint32_t(j0 + lane);
       if (p.idxmap) p.idxmap[j0 + lane] = myi;
     }
-    sidx[wid][lane] = myi;
+    if (lane < kTile) sidx[wid][lane] = myi;
     __syncwarp();
     // gather: element e = (row e / Q, float4 e % Q); eight independent 16-B loads in flight per lane
     for (uint32_t e0 = lane; e0 < nr * Q; e0 += 32 * 8) {

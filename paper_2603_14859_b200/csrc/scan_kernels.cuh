@@ -90,6 +90,11 @@ struct Shape {
 #else
   static constexpr int MINB = ((LP * R <= 96) ? 16 : 8) / NW;
 #endif
+#ifdef VPET_MINB_ROT
+  static constexpr int MINB_ROT = VPET_MINB_ROT;
+#else
+  static constexpr int MINB_ROT = MINB * 7 / 8 > 0 ? MINB * 7 / 8 : 1;  // the rotated path's extra state
+#endif
   static constexpr size_t STAGE_FLOATS = size_t(T) * LP;
   // prefetched boxes of one super-tile: its own [lo; hi] then its kSuper tiles' (double buffered)
   static constexpr size_t BOXB_FLOATS = size_t(kSuper + 1) * 2 * LP;
@@ -104,8 +109,9 @@ struct Shape {
   // top of each voxel's candidate heap (root + its 8 children) kept in shared memory per item
   static constexpr int KTOP = 9;
   static constexpr size_t HTOP_BYTES = VPET_SHEAP ? size_t(NT) * R * KTOP * 8 : 0;
+  static constexpr size_t RV_BYTES = size_t(NT) * R * 4;  // rotated basis: tail bounds per thread
   static constexpr size_t SMEM = REGION + size_t(NST) * T * 4 + NST * 8 + NST * 4 + NW * 4 + NW * LP * 4 + 16 + 64 +
-                                 size_t(kHyperSort) * 8 + 2 * BOXB_FLOATS * 4 + 16 + 16 + HTOP_BYTES + 16;
+                                 size_t(kHyperSort) * 8 + 2 * BOXB_FLOATS * 4 + 16 + 16 + HTOP_BYTES + 16 + RV_BYTES + 16;
 
 };
 
@@ -576,27 +582,83 @@ __device__ __forceinline__ void dist_range(const Voxels<LP, R>& V, const Src sr,
   }
 }
 
-// Rotated basis (WL2): the first kHead coordinates, then a warp test with the voxel's tail bound
-// rv: a row is dropped when fl(prefix + rv) >= tau_hi = tau (1 + 2 (LP + kHead + 4) u) (rounded up),
-// which implies D32 >= tau (the prefix is a FP32 sum of m + 1 terms, the rest of D32
-// adds terms >= the gaps summed in rv, and the whole sum rounds by at most gamma_{LP+1}).
+// Rotated basis (WL2): the first kHead coordinates, then a warp test against th = RU(RU(tau k) - rv),
+// rv the voxel's tail bound, k = 1 + 2 (LP + kHead + 4) u: a row is dropped when every lane's
+// prefix total is >= th, which implies D32 >= tau (the prefix is a FP32 sum of
+// kHead / 2 + 1 roundings per chain, the rest of D32 adds terms >= the gaps summed in rv, and the
+// whole sum rounds by at most (1 - u)^(LP / 2 + 1)).  th is computed per tile from the tau of the
+// tile's start (a larger, older tau only keeps more rows).
+constexpr float rot_tau_factor(int LP) { return 1.0f + float(2 * (LP + kHead + 4)) * 5.9604644775390625e-8f; }
+template <int LP, int R>
+__device__ __forceinline__ void rot_thresholds(const ScanParams& p, const Voxels<LP, R>& V, uint32_t rv_s, float (&th)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float rv;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(rv) : "r"(rv_s + uint32_t(r) * NT * 4u));
+    th[r] = p.prune ? __fsub_ru(__fmul_ru(V.tau[r], rot_tau_factor(LP)), rv) : __int_as_float(0x7f800000);
+  }
+}
 template <int LP, int R, int DIST, bool COUNT, bool SH = false>
-__device__ __forceinline__ void eval_row_rot(const ScanParams& p, Voxels<LP, R>& V, const SmemSrc sr, uint64_t i,
-                                             uint32_t part, unsigned long long& work, uint32_t htop_s = 0) {
-  constexpr float kTauHi = 1.0f + float(2 * (LP + kHead + 4)) * 5.9604644775390625e-8f;  // exact: LP + kHead + 4 < 2^22
+__device__ __forceinline__ void eval_row_rot(const ScanParams& p, Voxels<LP, R>& V, const SmemSrc sr, uint32_t i_a,
+                                             uint32_t part, unsigned long long& work, uint32_t htop_s,
+                                             const float (&th)[R]) {
   Acc acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc_zero(acc[r]);
   dist_range<LP, R, DIST, 0, kHead>(V, sr, acc);
-  bool alive = !p.prune;
+  bool alive = false;
 #pragma unroll
-  for (int r = 0; r < R; ++r) alive |= __fadd_rn(acc_total(acc[r]), V.rv[r]) < __fmul_ru(V.tau[r], kTauHi);
+  for (int r = 0; r < R; ++r) alive |= acc_total(acc[r]) < th[r];
   const bool go = __any_sync(0xffffffffu, alive);
   if (COUNT && !VPET_COUNT_PUSH) work += uint64_t(kHead) * R;
   if (!go) return;
   dist_range<LP, R, DIST, kHead, LP>(V, sr, acc);
   if (COUNT && !VPET_COUNT_PUSH) work += uint64_t(LP - kHead) * R;
+  uint32_t i;  // the draw index, read from the ring only for rows that pass the test
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(i) : "r"(i_a));
   finish_row<LP, R, COUNT, SH>(p, V, acc, i, part, work, htop_s);
+}
+
+// Two consecutive rows (at shared addresses ra, ra + 4 LP): both heads, one vote for the pair,
+// then each row that passes its own vote is finished as in eval_row_rot.
+#ifndef VPET_RPAIR
+#define VPET_RPAIR 1
+#endif
+template <int LP, int R, int DIST, bool COUNT, bool SH = false>
+__device__ __forceinline__ void eval_pair_rot(const ScanParams& p, Voxels<LP, R>& V, uint32_t ra, uint32_t ia,
+                                              uint32_t part, unsigned long long& work, uint32_t htop_s,
+                                              const float (&th)[R]) {
+  Acc aa[R], ab[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    acc_zero(aa[r]);
+    acc_zero(ab[r]);
+  }
+  const SmemSrc sa{ra}, sb{ra + 4u * LP};
+  dist_range<LP, R, DIST, 0, kHead>(V, sa, aa);
+  dist_range<LP, R, DIST, 0, kHead>(V, sb, ab);
+  bool la = false, lb = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    la |= acc_total(aa[r]) < th[r];
+    lb |= acc_total(ab[r]) < th[r];
+  }
+  if (COUNT && !VPET_COUNT_PUSH) work += 2ull * kHead * R;
+  if (!__any_sync(0xffffffffu, la || lb)) return;
+  if (__any_sync(0xffffffffu, la)) {
+    dist_range<LP, R, DIST, kHead, LP>(V, sa, aa);
+    if (COUNT && !VPET_COUNT_PUSH) work += uint64_t(LP - kHead) * R;
+    uint32_t i;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(i) : "r"(ia));
+    finish_row<LP, R, COUNT, SH>(p, V, aa, i, part, work, htop_s);
+  }
+  if (__any_sync(0xffffffffu, lb)) {
+    dist_range<LP, R, DIST, kHead, LP>(V, sb, ab);
+    if (COUNT && !VPET_COUNT_PUSH) work += uint64_t(LP - kHead) * R;
+    uint32_t i;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(i) : "r"(ia + 4u));
+    finish_row<LP, R, COUNT, SH>(p, V, ab, i, part, work, htop_s);
+  }
 }
 
 // Two rows at once: their first chunks run interleaved (twice the independent FMA chains, one
@@ -683,6 +745,53 @@ __device__ __forceinline__ bool box_alive(const Voxels<LP, R>& V, const SmemSrc 
   for (int r = 0; r < R; ++r) acc_zero(acc[r]);
   return Chunks<LP, R, DIST, true, 0>::run(V, box, box.off(LP), acc, work, false);
 }
+
+// Coordinates [Q0, Q1) of the box lower bound (WL2), as bound_chunk.
+template <int LP, int R, int Q0, int Q1, class Src>
+__device__ __forceinline__ void bound_range(const Voxels<LP, R>& V, const Src lo, const Src hi, Acc (&acc)[R]) {
+#pragma unroll
+  for (int q = Q0; q < Q1; q += 4) {
+    const float4 l4 = lo.ld(q);
+    const float4 h4 = hi.ld(q);
+    const float2 la = make_float2(l4.x, l4.y), lc = make_float2(l4.z, l4.w);
+    const float2 ha = make_float2(h4.x, h4.y), hc = make_float2(h4.z, h4.w);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float2 a0 = __fadd2_rn(V.y[r][q / 2], la), b0 = __fadd2_rn(V.y[r][q / 2], ha);
+      float2 a1 = __fadd2_rn(V.y[r][q / 2 + 1], lc), b1 = __fadd2_rn(V.y[r][q / 2 + 1], hc);
+      float2 g0 = make_float2(fmaxf(fmaxf(a0.x, -b0.x), 0.0f), fmaxf(fmaxf(a0.y, -b0.y), 0.0f));
+      float2 g1 = make_float2(fmaxf(fmaxf(a1.x, -b1.x), 0.0f), fmaxf(fmaxf(a1.y, -b1.y), 0.0f));
+      acc[r].a = __ffma2_rn(g0, g0, acc[r].a);
+      acc_second(acc[r]) = __ffma2_rn(g1, g1, acc_second(acc[r]));
+    }
+  }
+}
+
+// Rotated basis: the box's first kHead coordinates tested against th (as eval_row_rot: every
+// draw of the box then has D32 >= tau), then the whole lower bound against tau.
+template <int LP, int R, class Src>
+__device__ __forceinline__ bool box_alive_rot(const Voxels<LP, R>& V, const Src box, const float (&th)[R],
+                                              unsigned long long& work) {
+  Acc acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc_zero(acc[r]);
+  bound_range<LP, R, 0, kHead>(V, box, box.off(LP), acc);
+  work += uint64_t(kHead) * R;
+  bool alive = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) alive |= acc_total(acc[r]) < th[r];
+  if (!__any_sync(0xffffffffu, alive)) return false;
+  bound_range<LP, R, kHead, LP>(V, box, box.off(LP), acc);
+  work += uint64_t(LP - kHead) * R;
+  alive = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) alive |= acc_total(acc[r]) < V.tau[r];
+  return __any_sync(0xffffffffu, alive);
+}
+
+// th[r] = RU(RU(tau k) - rv) (eval_row_rot), +inf without pruning
+template <int LP, int R>
+__device__ __forceinline__ void rot_thresholds(const ScanParams& p, const Voxels<LP, R>& V, uint32_t rv_s, float (&th)[R]);
 
 template <int LP, int R>
 __device__ __forceinline__ void store_counts(const ScanParams& p, const Voxels<LP, R>& V, uint32_t part,
@@ -865,7 +974,7 @@ __device__ __forceinline__ float mean_lb(const float* yb, const float* lo) {
 // Tree scan: Morton-ordered bank, hyper-tile / super-tile / tile bounds, best-first order.
 // =============================================================================================
 template <int LP, int DIST, bool COUNT, bool ROT = false>
-__global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const ScanParams p) {
+__global__ void __launch_bounds__(NT, ROT ? Shape<LP>::MINB_ROT : Shape<LP>::MINB) scan_tree_kernel(const ScanParams p) {
   constexpr int R = Shape<LP>::R;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage = reinterpret_cast<float*>(smem_raw);  // [NST][STAGE_FLOATS] TMA ring
@@ -890,9 +999,13 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
   float* bbuf = reinterpret_cast<float*>(smem_raw + align16(sorder + kHyperSort));  // [2][BXF]
   uint64_t* bbar = reinterpret_cast<uint64_t*>(bbuf + 2 * BXF);                    // [2]
   const uint32_t stage_a = smem_u32(stage), bbuf_a = smem_u32(bbuf);  // 32-bit shared addresses
+  const uint32_t sidx_a = smem_u32(sidx);
   unsigned long long* htop = reinterpret_cast<unsigned long long*>(smem_raw + align16(bbar + 2));  // [R][NT][9]
   unsigned long long* htop_t = VPET_SHEAP ? htop + threadIdx.x * 9 : nullptr;
   const uint32_t htop_s = smem_u32(htop) + uint32_t(threadIdx.x) * 72u;  // this thread's heap tops (bytes)
+  // rotated basis: this thread's tail bounds rv[R] ([R][NT] floats after the heap tops)
+  const uint32_t rv_s = uint32_t(align16(reinterpret_cast<unsigned char*>(htop) + Shape<LP>::HTOP_BYTES)) +
+                        smem_u32(smem_raw) + uint32_t(threadIdx.x) * 4u;
 
   if (p.bad && *p.bad) return;  // non-finite TACs: the call fails with ABC_E_ARG, skip the work
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -959,6 +1072,11 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
     const uint64_t nsub = (p.nhyper > part) ? (p.nhyper - part + S - 1) / S : 0;  // hyper-tiles of this part
     Voxels<LP, R> V;
     load_voxels<LP, R, ROT>(p, V, tid, vt);
+    if constexpr (ROT) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(rv_s + uint32_t(r) * NT * 4u), "f"(V.rv[r]) : "memory");
+    }
 
     // ---- best-first order of this part's hyper-tiles: key = min over warps of the lower bound of
     // the warp's mean TAC against the hyper-tile box (a heuristic order; exactness does not depend
@@ -1003,7 +1121,14 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
     for (uint32_t q = 0; q < nsub; ++q) {
       const uint64_t h = part + uint64_t(horder[q]) * S;
       if ((q & VPET_HREFRESH) == 0) refresh_tau<LP, R>(p, V);
-      const bool halive = box_alive<LP, R, DIST>(V, GmemSrc{p.hbounds + h * 2 * LP}, bwork);
+      bool halive;
+      if constexpr (ROT) {
+        float thh[R];
+        rot_thresholds<LP, R>(p, V, rv_s, thh);
+        halive = box_alive_rot<LP, R>(V, GmemSrc{p.hbounds + h * 2 * LP}, thh, bwork);
+      } else {
+        halive = box_alive<LP, R, DIST>(V, GmemSrc{p.hbounds + h * 2 * LP}, bwork);
+      }
       if (!__syncthreads_or(halive)) continue;
       const uint64_t s0 = h * p.hs;
       const uint32_t ns = uint32_t(((s0 + p.hs < p.nsuper) ? s0 + p.hs : p.nsuper) - s0);
@@ -1028,7 +1153,11 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       ++bcount;
       // super-tile bound
       const uint32_t sbx_a = bbuf_a + cur * uint32_t(BXF) * 4u;  // shared address of the boxes
-      bool alive = halive && box_alive<LP, R, DIST>(V, SmemSrc{sbx_a}, bwork);
+      float ths[R];
+      if constexpr (ROT) rot_thresholds<LP, R>(p, V, rv_s, ths);
+      bool alive;
+      if constexpr (ROT) alive = halive && box_alive_rot<LP, R>(V, SmemSrc{sbx_a}, ths, bwork);
+      else alive = halive && box_alive<LP, R, DIST>(V, SmemSrc{sbx_a}, bwork);
 #ifdef VPET_TRAV_STATS
       if (tid == 0) atomicAdd(p.work + 1, 1ull << 32);  // super-tiles bound-checked (high word of bound_work)
 #endif
@@ -1039,7 +1168,8 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
       uint32_t mask = 0;
       if (alive) {
         for (uint64_t t = t0; t < t1; ++t)
-          if (box_alive<LP, R, DIST>(V, SmemSrc{sbx_a + 4u * uint32_t(2 * LP + (t - t0) * 2 * LP)}, bwork))
+          if (ROT ? box_alive_rot<LP, R>(V, SmemSrc{sbx_a + 4u * uint32_t(2 * LP + (t - t0) * 2 * LP)}, ths, bwork)
+                  : box_alive<LP, R, DIST>(V, SmemSrc{sbx_a + 4u * uint32_t(2 * LP + (t - t0) * 2 * LP)}, bwork))
             mask |= 1u << uint32_t(t - t0);
       }
 #ifdef VPET_UNION_STATS
@@ -1110,7 +1240,10 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
           if (VPET_TREFRESH == 2) refresh_tau<LP, R>(p, V);
           if (VPET_TREFRESH == 3) refresh_apply<LP, R>(V, gnow);
           const uint32_t sb_a = stage_a + uint32_t(st) * uint32_t(Shape<LP>::STAGE_FLOATS) * 4u;
+          float th[R];  // rotated basis: per-tile row threshold (eval_row_rot)
+          if constexpr (ROT) rot_thresholds<LP, R>(p, V, rv_s, th);
           const uint32_t* si = sidx + st * T;
+          const uint32_t si_a = sidx_a + 4u * uint32_t(st * T);  // shared address of si
           const uint64_t rem = N - t * T;
           const uint32_t nd = uint32_t(rem < uint64_t(T) ? rem : uint64_t(T));
 #ifndef VPET_PAIR
@@ -1127,7 +1260,7 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
             const uint32_t d0 = nd < kTrefreshRows ? nd : kTrefreshRows;
             for (; d < d0; ++d)
               {
-              if constexpr (ROT) eval_row_rot<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
+              if constexpr (ROT) eval_row_rot<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si_a + 4u * d, part, work, htop_s, th);
               else eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
             }
             refresh_apply<LP, R>(V, gnow4);
@@ -1137,11 +1270,18 @@ __global__ void __launch_bounds__(NT, Shape<LP>::MINB) scan_tree_kernel(const Sc
               eval_pair<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d],
                                                               SmemSrc{sb_a + 4u * (d + 1) * LP}, si[d + 1],
                                                               part, work, htop_s);
-          for (; d < nd; ++d)
-            {
-              if constexpr (ROT) eval_row_rot<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
-              else eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
-            }
+          if constexpr (ROT) {
+            // row addresses as induction variables (keeps the shared base out of the loop)
+            uint32_t ra = sb_a + 4u * d * LP, ia = si_a + 4u * d;
+            if (VPET_RPAIR)
+              for (; d + 1 < nd; d += 2, ra += 8u * LP, ia += 8u)
+                eval_pair_rot<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, ra, ia, part, work, htop_s, th);
+            for (; d < nd; ++d, ra += 4u * LP, ia += 4u)
+              eval_row_rot<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{ra}, ia, part, work, htop_s, th);
+          } else {
+            for (; d < nd; ++d)
+              eval_row<LP, R, DIST, COUNT, VPET_SHEAP != 0>(p, V, SmemSrc{sb_a + 4u * d * LP}, si[d], part, work, htop_s);
+          }
         }
         __syncwarp();
         if (lane == 0) {
@@ -1206,11 +1346,11 @@ cudaError_t launch_one(const ScanParams& p, cudaStream_t st) {
 
 template <int DIST>
 cudaError_t launch_dist(const ScanParams& p, uint32_t LP, int count_work, int tree, cudaStream_t st) {
-  // rotated basis (p.ytr): WL2, kHead < LP <= 64 (api.cu selects it only there)
+  // rotated basis (p.ytr): WL2, kHead < LP (api.cu selects it only for WL2)
   const bool rot = p.ytr != nullptr;
 #define X(v)                                                                          \
   if (LP == v) {                                                                      \
-    if constexpr (DIST == ABC_DIST_WL2 && v > kHead && v <= 64) {                     \
+    if constexpr (DIST == ABC_DIST_WL2 && v > kHead) {                                \
       if (tree && rot)                                                                \
         return count_work ? launch_one<v, DIST, true, true, true>(p, st) : launch_one<v, DIST, false, true, true>(p, st); \
     }                                                                                 \

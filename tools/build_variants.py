@@ -50,6 +50,16 @@ VARIANTS = {
     "npc3": ("VPET_NPC=3",),
     "npc5": ("VPET_NPC=5",),
     "quota0": ("VPET_QUOTA=0",),
+    "rpair0": ("VPET_RPAIR=0",),
+    "head4": ("VPET_HEAD=4",),
+    "head12": ("VPET_HEAD=12",),
+    "minb7": ("VPET_MINB=7",),
+    "rtr3": ("VPET_TREFRESH=3",),
+    "rtile16": ("VPET_TILE=16",),
+    "rsuper4": ("VPET_SUPER=4",),
+    "rsuper16": ("VPET_SUPER=16",),
+    "rchb8": ("VPET_CHB=8",),
+    "rchb16": ("VPET_CHB=16",),
     "r1ch12": ("VPET_R=1", "VPET_CH=12"),
     "r1ch16": ("VPET_R=1", "VPET_CH=16"),
     "r1ch36": ("VPET_R=1", "VPET_CH=36"),
