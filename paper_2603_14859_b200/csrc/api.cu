@@ -103,6 +103,8 @@ struct abc_ctx {
   cudaEvent_t ev[EV_N] = {};
   cudaStream_t copy = nullptr;       // host->device TAC copies, overlapped with the bank / order stages
   cudaEvent_t tacs_ready = nullptr;
+  cudaStream_t aux = nullptr;        // the order stage's basis computation, overlapped with its sorts
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool ev_ok = false;
   int num_sms = 148;
 };
@@ -415,9 +417,26 @@ uint32_t scan_lp_for(uint32_t L) {
 
 namespace {
 
-__global__ void finite_check_kernel(const float* x, uint64_t n, int* flag) {
-  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x)
-    if (!isfinite(x[e])) *flag = 1;
+// 16-B loads, four in flight per thread (the TAC buffer is cudaMalloc- or user-aligned to 16 B when
+// its size allows; otherwise the scalar loop covers everything)
+__global__ void __launch_bounds__(256) finite_check_kernel(const float* x, uint64_t n, int* flag) {
+  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, nt = uint64_t(gridDim.x) * blockDim.x;
+  bool bad = false;
+  uint64_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const uint64_t n4 = n / 4;
+    for (uint64_t e = tid; e < n4; e += 4 * nt) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = e + u * nt < n4 ? __ldcs(x4 + e + u * nt) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bad |= !(isfinite(v[u].x) && isfinite(v[u].y) && isfinite(v[u].z) && isfinite(v[u].w));
+    }
+    done = n4 * 4;
+  }
+  for (uint64_t e = done + tid; e < n; e += nt) bad |= !isfinite(x[e]);
+  if (bad) *flag = 1;
 }
 
 }  // namespace
@@ -490,7 +509,10 @@ abc_status abc_init(const abc_config* cfg, abc_ctx** out) {
   }
   c->stream = c->own;
   if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->tacs_ready, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->tacs_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     cudaStreamDestroy(c->own);
     delete c;
     return ABC_E_CUDA;
@@ -647,9 +669,10 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (dense) need += dense_bank_bytes(N) + dense_voxel_bytes(J) + 4 * J;
   const bool tree = !exact && !dense && !(ctx->cfg.flags & ABC_FLAG_NO_TREE) && N < (1ull << 31);
   const uint64_t ntile = (N + kTile - 1) / kTile, nsuper = (ntile + kSuper - 1) / kSuper;
-  // rotated scan basis: WL2, tree mode, frame reordering allowed
+  // rotated scan basis: WL2, tree mode, frame reordering allowed, LP <= 96 (shared
+  // memory of the basis and rotation kernels)
   static const bool rot_env = getenv("VPET_ROT") ? atoi(getenv("VPET_ROT")) != 0 : true;  // tuning knob
-  const bool rotated = rot_env && tree && ctx->dist_wl2() && !(ctx->cfg.flags & ABC_FLAG_NO_REORDER);
+  const bool rotated = rot_env && tree && ctx->dist_wl2() && !(ctx->cfg.flags & ABC_FLAG_NO_REORDER) && LP <= 96;
   const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
   // draw-range split of the tree scan (interleaved super-tiles): balances heavy voxels over SMs
   uint32_t nparts = 1;
@@ -835,7 +858,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       cudaError_t e = cudaStreamWaitEvent(st, ctx->tacs_ready, 0);
       if (e != cudaSuccess) return e;
     }
-    finite_check_kernel<<<148, 256, 0, st>>>(d_tacs, J * L, ctx->flag.as<int>());
+    finite_check_kernel<<<148 * 8, 256, 0, st>>>(d_tacs, J * L, ctx->flag.as<int>());
     ++launches;
     return cudaGetLastError();
   };
@@ -885,6 +908,9 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
         op.rotq = ctx->rotq.as<double>();
         op.cw = ctx->d_cwd.as<double>();
         op.gbox = ctx->gbox.as<float>();
+        op.aux = ctx->aux;
+        op.ev_fork = ctx->ev_fork;
+        op.ev_join = ctx->ev_join;
       }
     }
     CK(launch_order(op, st, &launches));
@@ -1422,6 +1448,9 @@ void abc_destroy(abc_ctx* ctx) {
     if (ctx->ev[k]) cudaEventDestroy(ctx->ev[k]);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->tacs_ready) cudaEventDestroy(ctx->tacs_ready);
   delete ctx;
 }

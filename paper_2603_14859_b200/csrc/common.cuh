@@ -237,6 +237,8 @@ struct OrderParams {
   double* rotq;         // [L][LP] out: rotq[f][k] = Q[a][k] sqrt(w_f), f = perm[a]; scan coordinate k = sum_f rotq[f][k] x_f
   const double* cw;     // [L] sqrt(w_f) in FP64 (1 for unit weights)
   float* gbox;          // [2][LP] out (rotated basis): min / max of bankp over all draws
+  cudaStream_t aux;     // if set: the basis (rot_kernel) runs on it, overlapped with the draw-order sort
+  cudaEvent_t ev_fork, ev_join;
 };
 cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launches);
 // Rotated voxel coordinates ytr[j][k] = RN32(sum_f rotq[f][k] y_f) (FP64 sums), k < LP.

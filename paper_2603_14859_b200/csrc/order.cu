@@ -117,14 +117,12 @@ __global__ void __launch_bounds__(256) cov_kernel(const OrderParams p) {
 // ---- first kNPC principal axes of the covariance: power iteration with deflation, one warp;
 // stops when the direction changes by < 1e-9 (eigen-gaps of a bank are large) or after 100 steps ----
 __global__ void __launch_bounds__(32) pca_kernel(const OrderParams p) {
-  __shared__ double C[kMaxLP * kMaxLP / 4];  // LP <= 64; larger LP works from global memory
+  extern __shared__ double C[];  // [LP][LP] working copy (p.cov stays intact for rot_kernel)
   __shared__ double v[kMaxLP], w[kMaxLP];
   const uint32_t LP = p.LP;
   const int lane = threadIdx.x;
-  const bool in_smem = LP * LP <= kMaxLP * kMaxLP / 4;
-  double* Cm = in_smem ? C : p.cov;
-  if (in_smem)
-    for (uint32_t e = lane; e < LP * LP; e += 32) C[e] = p.cov[e];
+  double* Cm = C;
+  for (uint32_t e = lane; e < LP * LP; e += 32) C[e] = p.cov[e];
   __syncwarp();
   auto wsum = [](double x) {
 #pragma unroll
@@ -177,7 +175,7 @@ __global__ void __launch_bounds__(32) pca_kernel(const OrderParams p) {
 // the variance), so in this basis a tile's box is thin in every coordinate.
 // Exactness does not rest on Q being eigenvectors, only on its orthogonality, which is checked:
 // LP * max|Q^T Q - I| > kRotEps falls back to Q = I. ----
-constexpr uint32_t kRotMaxLP = kMaxLP;
+constexpr uint32_t kRotMaxLP = 96;  // shared memory: rot_kernel 2 LP^2 doubles, permute LP L doubles + rows
 __global__ void __launch_bounds__(256) rot_kernel(const OrderParams p) {
   extern __shared__ double rsm[];
   const uint32_t n = p.LP;  // a multiple of 4
@@ -484,6 +482,36 @@ __global__ void __launch_bounds__(256) key_kernel(const OrderParams p) {
   }
 }
 
+// Rotated coordinates of one curve x (L floats, shared memory) into out (LP floats): RN32 of the FP64
+// sums over the frames, in blocks of KB coordinates (one pass over x per block), negated if NEG.
+template <int KB, bool NEG>
+__device__ __forceinline__ uint32_t rotate_blocks(const float* x, const double* q, uint32_t L, uint32_t LP, uint32_t k0,
+                                                  float* out) {
+  for (; k0 + KB <= LP; k0 += KB) {
+    double acc[KB];
+#pragma unroll
+    for (int u = 0; u < KB; ++u) acc[u] = 0.0;
+    for (uint32_t f = 0; f < L; ++f) {
+      const double xf = double(x[f]);
+      const double2* qf = reinterpret_cast<const double2*>(q + f * LP + k0);
+#pragma unroll
+      for (int u = 0; u < KB / 2; ++u) {
+        const double2 c = qf[u];
+        acc[2 * u] = fma(c.x, xf, acc[2 * u]);
+        acc[2 * u + 1] = fma(c.y, xf, acc[2 * u + 1]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < KB; ++u) out[k0 + u] = NEG ? -__double2float_rn(acc[u]) : __double2float_rn(acc[u]);
+  }
+  return k0;
+}
+template <bool NEG>
+__device__ __forceinline__ void rotate_curve(const float* x, const double* q, uint32_t L, uint32_t LP, float* out) {
+  uint32_t k0 = rotate_blocks<12, NEG>(x, q, L, LP, 0, out);
+  rotate_blocks<4, NEG>(x, q, L, LP, k0, out);
+}
+
 // ---- scan-order copy fused with the tile bounds, one warp per tile of kTile rows:
 // bankp[j][k] = -(wsp[k] * bank[order[j]][perm[k]]), idxmap[j] = order[j], and (tree mode)
 // tbounds[t] = per-frame [min, max] of the tile's bankp rows.  Raw rows are gathered with
@@ -542,21 +570,7 @@ __global__ void __launch_bounds__(32 * kPermWarps) permute_kernel(const OrderPar
       // rotated basis: lane r computes row r's LP coordinates, RN32 of FP64 sums over the frames,
       // into its own row of rows (overwritten in place after the whole row is read), negated
       float* orows = rows + kTile * stride;  // [kTile][stride] rotated rows of this warp
-      if (uint32_t(lane) < nr) {
-        const float* row = rows + lane * stride;
-        float* orow = orows + lane * stride;
-        for (uint32_t k0 = 0; k0 < p.LP; k0 += 4) {
-          double acc[4] = {0.0, 0.0, 0.0, 0.0};
-          for (uint32_t f = 0; f < p.L; ++f) {
-            const double x = double(row[f]);
-            const double* q = srot + f * p.LP + k0;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] = fma(q[u], x, acc[u]);
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) orow[k0 + u] = -__double2float_rn(acc[u]);
-        }
-      }
+      if (uint32_t(lane) < nr) rotate_curve<true>(rows + lane * stride, srot, p.L, p.LP, orows + lane * stride);
       __syncwarp();
       for (uint32_t q = lane; q < nr * QP; q += 32) {
         const float* row = orows + (q / QP) * stride + 4 * (q % QP);
@@ -724,25 +738,32 @@ __global__ void __launch_bounds__(256) voxel_key_kernel(const VoxelOrderParams p
   }
 }
 
-// ---- rotated voxel coordinates: thread per voxel, ytr[j][k] = RN32(sum_f rotq[f][k] y_f) ----
-__global__ void __launch_bounds__(128) voxel_rotate_kernel(const float* __restrict__ tacs, uint64_t J, uint32_t L,
+// ---- rotated voxel coordinates: thread per voxel, ytr[j][k] = RN32(sum_f rotq[f][k] y_f); the
+// block's TAC rows are staged in shared memory with coalesced loads (odd row stride) ----
+constexpr int kVR = 128;
+__global__ void __launch_bounds__(kVR) voxel_rotate_kernel(const float* __restrict__ tacs, uint64_t J, uint32_t L,
                                                            uint32_t LP, const double* __restrict__ rotq,
                                                            float* __restrict__ ytr) {
-  extern __shared__ double vq[];  // [L][LP]
-  for (uint32_t e = threadIdx.x; e < L * LP; e += blockDim.x) vq[e] = rotq[e];
-  __syncthreads();
-  for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < J; j += uint64_t(gridDim.x) * blockDim.x) {
-    const float* y = tacs + j * L;
-    float4* out = reinterpret_cast<float4*>(ytr + j * LP);
-    for (uint32_t k0 = 0; k0 < LP; k0 += 4) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (uint32_t f = 0; f < L; ++f) {
-        const double x = double(__ldg(y + f));
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] = fma(vq[f * LP + k0 + u], x, acc[u]);
-      }
-      out[k0 / 4] = make_float4(__double2float_rn(acc[0]), __double2float_rn(acc[1]), __double2float_rn(acc[2]),
-                                __double2float_rn(acc[3]));
+  extern __shared__ double vq[];  // [L][LP] rotq, then [kVR][ys] TAC rows, then [kVR][LP + 1] outputs
+  const uint32_t ys = L | 1u, os = LP + 1;
+  float* yb = reinterpret_cast<float*>(vq + L * LP);
+  float* ob = yb + kVR * ys;
+  for (uint32_t e = threadIdx.x; e < L * LP; e += kVR) vq[e] = rotq[e];
+  for (uint64_t base = uint64_t(blockIdx.x) * kVR; base < J; base += uint64_t(gridDim.x) * kVR) {
+    const uint32_t nb = uint32_t(J - base < uint64_t(kVR) ? J - base : uint64_t(kVR));
+    __syncthreads();
+    const float* src = tacs + base * L;
+    for (uint32_t e = threadIdx.x; e < nb * L; e += kVR) {
+      const uint32_t v = e / L;
+      yb[v * ys + (e - v * L)] = __ldcs(src + e);
+    }
+    __syncthreads();
+    if (threadIdx.x < nb) rotate_curve<false>(yb + threadIdx.x * ys, vq, L, LP, ob + threadIdx.x * os);
+    __syncthreads();
+    float* dst = ytr + base * LP;  // the block's rows are contiguous: coalesced stores
+    for (uint32_t e = threadIdx.x; e < nb * LP; e += kVR) {
+      const uint32_t v = e / LP;
+      dst[e] = ob[v * os + (e - v * LP)];
     }
   }
 }
@@ -752,10 +773,10 @@ __global__ void __launch_bounds__(128) voxel_rotate_kernel(const float* __restri
 cudaError_t launch_voxel_rotate(const float* tacs, uint64_t J, uint32_t L, uint32_t LP, const double* rotq, float* ytr,
                                 cudaStream_t st) {
   if (LP > kRotMaxLP) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(double) * L * LP;
+  const size_t smem = sizeof(double) * L * LP + sizeof(float) * kVR * ((L | 1u) + LP + 1);
   cudaError_t e = ensure_smem_attr((const void*)voxel_rotate_kernel, smem);
   if (e != cudaSuccess) return e;
-  voxel_rotate_kernel<<<148 * 8, 128, smem, st>>>(tacs, J, L, LP, rotq, ytr);
+  voxel_rotate_kernel<<<148 * 4, kVR, smem, st>>>(tacs, J, L, LP, rotq, ytr);
   return cudaGetLastError();
 }
 
@@ -780,18 +801,31 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
   if (p.tree) {
     cudaMemsetAsync(p.cov, 0, sizeof(double) * p.LP * p.LP, st);
     cov_kernel<<<dim3(p.LP, p.LP), 256, 0, st>>>(p);
-    pca_kernel<<<1, 32, 0, st>>>(p);
-    proj_minmax_kernel<<<148 * 4, 256, 0, st>>>(p);
-    key_kernel<<<148 * 8, 256, 0, st>>>(p);
-    *launches += 4;
-    if (p.rotq) {
+    *launches += 2;
+    if (p.rotq) {  // needs cov only; with an aux stream it overlaps proj / key / sort
       if (p.LP > kRotMaxLP) return cudaErrorInvalidValue;
       const size_t rs = sizeof(double) * 2 * p.LP * p.LP;
       cudaError_t er = ensure_smem_attr((const void*)rot_kernel, rs);
       if (er != cudaSuccess) return er;
-      rot_kernel<<<1, 256, rs, st>>>(p);
+      cudaStream_t rst = st;
+      if (p.aux) {
+        cudaEventRecord(p.ev_fork, st);
+        cudaStreamWaitEvent(p.aux, p.ev_fork, 0);
+        rst = p.aux;
+      }
+      rot_kernel<<<1, 256, rs, rst>>>(p);
+      if (p.aux) cudaEventRecord(p.ev_join, p.aux);
       *launches += 1;
     }
+    {
+      const size_t cs = sizeof(double) * p.LP * p.LP;
+      cudaError_t ec = ensure_smem_attr((const void*)pca_kernel, cs);
+      if (ec != cudaSuccess) return ec;
+      pca_kernel<<<1, 32, cs, st>>>(p);
+    }
+    proj_minmax_kernel<<<148 * 4, 256, 0, st>>>(p);
+    key_kernel<<<148 * 8, 256, 0, st>>>(p);
+    *launches += 2;
     // the lowest 8 key bits (the two finest levels of the curve) are not sorted: one radix pass
     // less, same scan time (Morton, measured: 0 / 8 / 16 bits -> scan 19.6 / 19.5 / 20.3 ms; with
     // the Hilbert order 24 unsorted bits double the scan); the order is free.
@@ -805,6 +839,7 @@ cudaError_t launch_order(const OrderParams& p, cudaStream_t st, uint32_t* launch
   }
   {
     if (!p.tree) q.rotq = nullptr;
+    if (q.rotq && p.aux) cudaStreamWaitEvent(st, p.ev_join, 0);
     const size_t psmem = sizeof(float) * kPermWarps * kTile * ((p.LS > p.LP ? p.LS : p.LP) + 1) * (q.rotq ? 2 : 1) +
                          (q.rotq ? sizeof(double) * p.L * p.LP : 0);
     cudaError_t ea = ensure_smem_attr((const void*)permute_kernel, psmem);
