@@ -89,7 +89,7 @@ struct abc_ctx {
   DevBuf d_prior, bank, bankp, var, fmean, perm, wsp, heap, heap_cnt, tacs, fb_list, fb_len, work, hd, hidx, mom, flag, outs;
   DevBuf cov, pcs, pminmax, keys, keys_alt, vals, order, idxmap, sort_temp, tbounds, sbounds, hbounds, tau_glob, queue;
   DevBuf rotq, ytr, gbox;  // rotated scan basis: [L][LP] FP64 rotation, [J][LP] voxel coordinates, [2][LP] bank box
-  DevBuf vkeys, vkeys_alt, vvals, vorder, vsort_temp, item_log;
+  DevBuf vkeys, vkeys_alt, vvals, vorder, vslot, vsort_temp, item_log;
   DevBuf fb_tau, cl_d, cl_i, cl_cnt, fb2_list, fb2_len;  // fallback tiers (certify.cu)
   DevBuf dBt, dS2, dAt, dY2;  // ABC_FLAG_DENSE_TC operands (dense_tc.cu)
   DevBuf env_idx, env_t, env_q;  // abc_response_envelope staging
@@ -706,7 +706,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   if (dense) nparts = 2;  // the two column halves of each draw tile (dense_tc.cu)
   const size_t vsort_tmp = tree ? voxel_sort_temp_bytes(J) : 0;
   if (tree) need += N * (8 + 8 + 4 + 4 + 4 + 4 * kNPC) + 16 + sort_tmp + sizeof(float) * 2 * LP * (ntile + nsuper + nhyper);
-  if (tree) need += 24 * J + vsort_tmp;
+  if (tree) need += 28 * J + vsort_tmp;
   if (rotated) need += sizeof(double) * L * LP + sizeof(float) * J * LP;
   if (!eps) need += (size_t(8) * heap_stride(std::max<uint32_t>(K, 1)) + 4) * J * nparts + 4 * J;  // heaps
   need += size_t(12) * J * (n ? n : 1);                  // exact heaps (last-resort fallback)
@@ -772,6 +772,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     CK(ctx->vkeys_alt.ensure(8 * J));
     CK(ctx->vvals.ensure(4 * J));
     CK(ctx->vorder.ensure(4 * J));
+    CK(ctx->vslot.ensure(4 * J));
     CK(ctx->vsort_temp.ensure(vsort_tmp));
   }
   CK(ctx->perm.ensure(sizeof(int) * kMaxLP));
@@ -930,6 +931,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
       vp.keys_alt = ctx->vkeys_alt.as<unsigned long long>();
       vp.vals = ctx->vvals.as<uint32_t>();
       vp.vorder = ctx->vorder.as<uint32_t>();
+      vp.vslot = ctx->vslot.as<uint32_t>();
       vp.sort_temp = ctx->vsort_temp.p;
       vp.sort_temp_bytes = vsort_tmp;
       CK(launch_voxel_order(vp, st, &launches));
@@ -1032,6 +1034,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   rp.K = K;
   rp.nparts = ((tree || dense) && !eps) ? nparts : 1;
   rp.tau_glob = ((tree || dense) && !eps) ? ctx->tau_glob.as<unsigned int>() : nullptr;
+  rp.vslot = tree ? ctx->vslot.as<uint32_t>() : nullptr;  // tau_glob is slot-indexed in tree mode
   rp.heap = ctx->heap.as<unsigned long long>();
   rp.heap_cnt = ctx->heap_cnt.as<uint32_t>();
   rp.hd = ctx->hd.as<double>();
@@ -1433,7 +1436,7 @@ void abc_destroy(abc_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs2[] = {&ctx->fmean, &ctx->cov, &ctx->pcs, &ctx->pminmax, &ctx->keys, &ctx->keys_alt, &ctx->vals,
                      &ctx->order, &ctx->idxmap, &ctx->sort_temp, &ctx->tbounds, &ctx->sbounds, &ctx->hbounds, &ctx->tau_glob, &ctx->rotq, &ctx->ytr, &ctx->gbox,
-                     &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vsort_temp, &ctx->item_log,
+                     &ctx->queue, &ctx->vkeys, &ctx->vkeys_alt, &ctx->vvals, &ctx->vorder, &ctx->vslot, &ctx->vsort_temp, &ctx->item_log,
                      &ctx->dBt, &ctx->dS2, &ctx->dAt, &ctx->dY2,
                      &ctx->env_idx, &ctx->env_t, &ctx->env_q, &ctx->proj, &ctx->pat_ab,
                      &ctx->fb_tau, &ctx->cl_d, &ctx->cl_i, &ctx->cl_cnt, &ctx->fb2_list, &ctx->fb2_len};

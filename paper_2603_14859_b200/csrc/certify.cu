@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(256, CERT_MINB) certify_reduce_kernel(const Re
       uint64_t total = 0;
       for (uint32_t q = 0; q < S; ++q) total += p.heap_cnt[v * S + q];
       if (p.tau_glob) {
-        B = __uint_as_float(p.tau_glob[v]);
+        B = __uint_as_float(p.tau_glob[p.vslot ? p.vslot[v] : v]);
       } else if (p.heap_cnt[v] >= p.K) {
         float tmax = 0.0f;
         for (uint32_t a = lane; a < p.K; a += 32)
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(kLT, 2) certify_large_kernel(const ReduceParam
       uint64_t total = 0;
       for (uint32_t q = 0; q < S; ++q) total += p.heap_cnt[v * S + q];
       if (p.tau_glob) {
-        B = __uint_as_float(p.tau_glob[v]);
+        B = __uint_as_float(p.tau_glob[p.vslot ? p.vslot[v] : v]);
       } else if (p.heap_cnt[v] >= p.K) {  // flat mode: the root of the single heap is its maximum
         B = __uint_as_float(uint32_t(p.heap[v * heap_stride(p.K) + kHeapOff] >> 32));
       }

@@ -263,6 +263,7 @@ struct VoxelOrderParams {
   unsigned long long* keys_alt;
   uint32_t* vals;
   uint32_t* vorder;   // out [J]
+  uint32_t* vslot;    // out [J]: vslot[vorder[j]] = j
   void* sort_temp;
   size_t sort_temp_bytes;
 };
@@ -317,7 +318,7 @@ struct ScanParams {
   // work split: item = (voxel tile, part); part p owns hyper-tiles h = p (mod nparts) and its own
   // heap [J][nparts][K]; tau_glob[v] = min over parts of their heap thresholds (shared pruning)
   uint32_t nparts;
-  unsigned int* tau_glob;   // [J] float bits (positive), atomicMin
+  unsigned int* tau_glob;   // [J] float bits (positive), atomicMin; indexed by scan slot (vorder position)
   unsigned int* queue;      // work-queue counter (zeroed per run)
   unsigned long long* item_log;  // diagnostics (env VPET_ITEMLOG): [item][4] = start ns, end ns, SM, voxel tile
   const uint32_t* vorder;   // [J] voxel processed in slot j (tree mode) or nullptr (identity)
@@ -364,7 +365,8 @@ struct ReduceParams {
   const uint32_t* heap_cnt;        // [J][nparts]
   uint32_t K;
   uint32_t nparts;
-  const unsigned int* tau_glob;    // [J] (tree mode) or nullptr: bound B on excluded draws' D32
+  const unsigned int* tau_glob;    // [J] by scan slot (tree mode, via vslot) or voxel, or nullptr: bound B on excluded draws' D32
+  const uint32_t* vslot;           // [J] scan slot of voxel v (tree mode) or nullptr (identity)
   const double* hd;             // exact mode
   const uint32_t* hidx;
   const uint32_t* list;         // voxel list or nullptr

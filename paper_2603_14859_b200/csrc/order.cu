@@ -768,6 +768,11 @@ __global__ void __launch_bounds__(kVR) voxel_rotate_kernel(const float* __restri
   }
 }
 
+__global__ void vslot_kernel(const uint32_t* __restrict__ vorder, uint64_t J, uint32_t* __restrict__ vslot) {
+  for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < J; j += uint64_t(gridDim.x) * blockDim.x)
+    vslot[vorder[j]] = uint32_t(j);
+}
+
 }  // namespace
 
 cudaError_t launch_voxel_rotate(const float* tacs, uint64_t J, uint32_t L, uint32_t LP, const double* rotq, float* ytr,
@@ -788,6 +793,10 @@ cudaError_t launch_voxel_order(const VoxelOrderParams& p, cudaStream_t st, uint3
   cudaError_t e = radix_sort_pairs(p.sort_temp, p.sort_temp_bytes, p.keys, p.keys_alt, p.vals, p.vorder, p.J, 0,
                                    kVoxBits, st, launches);
   if (e != cudaSuccess) return e;
+  if (p.vslot) {
+    vslot_kernel<<<148 * 4, 256, 0, st>>>(p.vorder, p.J, p.vslot);
+    *launches += 1;
+  }
   return cudaGetLastError();
 }
 

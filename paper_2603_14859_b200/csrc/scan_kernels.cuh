@@ -298,6 +298,12 @@ static __device__ __noinline__ void eps_candidate(const float* yrow, const float
   }
 }
 
+// tau_glob is indexed by scan-order slot (a warp's 32 lanes read 32 consecutive words: one request)
+#ifndef VPET_WARP_CONTIG
+#define VPET_WARP_CONTIG 1
+#endif
+constexpr uint32_t kSlotStride = VPET_WARP_CONTIG ? 32u : uint32_t(NT);
+
 // Per-thread voxel state.
 template <int LP, int R>
 struct Voxels {
@@ -306,6 +312,7 @@ struct Voxels {
   float taup[R];  // own (part) heap root, +inf until the heap is full
   uint32_t cnt[R];
   uint32_t vox[R];  // voxel index (>= J for an empty slot)
+  uint32_t slot0;   // scan-order slot of voxel 0; voxel r sits at slot0 + r * kSlotStride
   float rv[R];      // rotated basis: lower bound on the coordinates >= kHead of every draw's D32 terms
 };
 
@@ -321,6 +328,7 @@ __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& 
     // is evaluated for all of them once its bound is alive for one)
     const uint64_t slot = VPET_WARP_CONTIG ? vtile * (NT * R) + uint64_t(tid >> 5) * (32 * R) + uint64_t(r) * 32 + (tid & 31)
                                            : vtile * (NT * R) + uint64_t(r) * NT + tid;
+    if (r == 0) V.slot0 = uint32_t(slot);
     bool valid = slot < p.J;
     uint64_t v = (valid && p.vorder) ? uint64_t(__ldg(p.vorder + slot)) : slot;
     V.vox[r] = uint32_t(v);
@@ -362,7 +370,7 @@ __device__ __forceinline__ void load_voxels(const ScanParams& p, Voxels<LP, R>& 
     V.taup[r] = INF;
     if (!p.eps_mode) {
       V.tau[r] = valid ? INF : -INF;
-      if (valid && p.tau_glob) V.tau[r] = fminf(V.tau[r], __uint_as_float(__ldcg(p.tau_glob + v)));
+      if (valid && p.tau_glob) V.tau[r] = fminf(V.tau[r], __uint_as_float(__ldcg(p.tau_glob + slot)));
     } else {
       double Y2 = 0.0, Y1 = 0.0;
       if (valid) {
@@ -529,7 +537,7 @@ __device__ __forceinline__ void finish_row(const ScanParams& p, Voxels<LP, R>& V
   for (int r = 0; r < R; ++r) {
     float D = acc_total(acc[r]);
     if (VPET_PUSHCHECK && D < V.tau[r] && !p.eps_mode && p.tau_glob)
-      V.tau[r] = fminf(V.tau[r], __uint_as_float(__ldcg(p.tau_glob + V.vox[r])));
+      V.tau[r] = fminf(V.tau[r], __uint_as_float(__ldcg(p.tau_glob + V.slot0 + uint32_t(r) * kSlotStride)));
     if (D < V.tau[r]) {
       if (!p.eps_mode) {
         unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(D)) << 32) | uint32_t(i);
@@ -542,7 +550,7 @@ __device__ __forceinline__ void finish_row(const ScanParams& p, Voxels<LP, R>& V
 #endif
         V.cnt[r] = st.x;
         V.taup[r] = __uint_as_float(st.y);
-        if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + V.vox[r], st.y);
+        if (p.tau_glob && st.y != 0x7f800000u) atomicMin(p.tau_glob + V.slot0 + uint32_t(r) * kSlotStride, st.y);
         V.tau[r] = fminf(V.tau[r], V.taup[r]);
       } else {
         eps_candidate(p.tacs + uint64_t(V.vox[r]) * p.L, p.bank, p.LS, p.w, p.L, p.dist, p.eps,
@@ -700,7 +708,7 @@ __device__ __forceinline__ void refresh_tau(const ScanParams& p, Voxels<LP, R>& 
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     if (V.vox[r] < p.J) {
-      float g = __uint_as_float(__ldcg(p.tau_glob + V.vox[r]));
+      float g = __uint_as_float(__ldcg(p.tau_glob + V.slot0 + uint32_t(r) * kSlotStride));
       V.tau[r] = fminf(V.tau[r], g);
     }
   }
@@ -711,7 +719,7 @@ template <int LP, int R>
 __device__ __forceinline__ void refresh_issue(const ScanParams& p, const Voxels<LP, R>& V, float (&g)[R]) {
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    g[r] = (!p.eps_mode && p.tau_glob && V.vox[r] < p.J) ? __uint_as_float(__ldcg(p.tau_glob + V.vox[r]))
+    g[r] = (!p.eps_mode && p.tau_glob && V.vox[r] < p.J) ? __uint_as_float(__ldcg(p.tau_glob + V.slot0 + uint32_t(r) * kSlotStride))
                                                           : __int_as_float(0x7f800000);
 }
 template <int LP, int R>
@@ -727,7 +735,7 @@ __device__ __forceinline__ void refresh_tau_pipe(const ScanParams& p, Voxels<LP,
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     V.tau[r] = fminf(V.tau[r], gpend[r]);
-    if (V.vox[r] < p.J) gpend[r] = __uint_as_float(__ldcg(p.tau_glob + V.vox[r]));
+    if (V.vox[r] < p.J) gpend[r] = __uint_as_float(__ldcg(p.tau_glob + V.slot0 + uint32_t(r) * kSlotStride));
   }
 }
 
