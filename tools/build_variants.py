@@ -51,6 +51,13 @@ VARIANTS = {
     "npc5": ("VPET_NPC=5",),
     "quota0": ("VPET_QUOTA=0",),
     "rpair0": ("VPET_RPAIR=0",),
+    "tr0": ("VPET_TREFRESH=0",),
+    "tr1": ("VPET_TREFRESH=1",),
+    "sheap1": ("VPET_SHEAP=1",),
+    "h12m6": ("VPET_HEAD=12", "VPET_MINB_ROT=6"),
+    "h12m8": ("VPET_HEAD=12", "VPET_MINB_ROT=8"),
+    "h12": ("VPET_HEAD=12",),
+    "tr0ref0": ("VPET_TREFRESH=0", "VPET_REFRESH=0"),
     "head4": ("VPET_HEAD=4",),
     "head12": ("VPET_HEAD=12",),
     "minb7": ("VPET_MINB=7",),
