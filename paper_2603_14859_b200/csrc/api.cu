@@ -680,12 +680,13 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   // fewer parts (certification holds all parts' candidates of a voxel in shared memory)
   // The parts also balance the persistent scan over the SMs: with few voxel tiles per CTA slot
   // more parts keep every SM busy, with many the parts only duplicate heap fills and threshold
-  // traffic.  Measured best on the TB phantom (CTA slots = SMs x 8): 6 parts at 0.96 voxel tiles per
-  // slot (1/32 slab set), 4 at 3.7 (1/8), 3 at 29 (the whole volume: 361 -> 319 ms vs 6 parts).
+  // traffic.  Measured best on the TB phantom with the rotated scan (CTA slots = SMs x 8): 4-6 parts
+  // at 1.8 voxel tiles per slot (1/16 slab set), 2 at 7.3 (1/4) and at 29 (the whole volume: 170 ms
+  // vs 173 with 1 part and 178 with 3; the frame-basis kernel wanted 6 / 4 / 3).
   if (tree && !eps) {
     if (K <= 512) {
       const double tiles_per_slot = double((J + 127) / 128) / double(std::max(1, ctx->num_sms) * 8);
-      nparts = tiles_per_slot < 2.0 ? 6u : (tiles_per_slot < 10.0 ? 4u : 3u);
+      nparts = tiles_per_slot < 2.0 ? 6u : (tiles_per_slot < 4.0 ? 4u : 2u);
     } else {
       nparts = 2 * K <= kLargeMaxCand ? 2u : 1u;
     }

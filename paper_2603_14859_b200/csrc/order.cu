@@ -666,10 +666,10 @@ __global__ void __launch_bounds__(128) global_box_kernel(const OrderParams p) {
 // Voxel scan order.  VPET_VOXKEY = 1: first-principal-axis projection; D = 2 or 4: D-dimensional
 // Morton code of the projection on the first D principal axes, on the bank's isotropic grid.
 #ifndef VPET_VOXKEY
-#define VPET_VOXKEY 3
+#define VPET_VOXKEY 4  // rotated scan: 4 axes on an isotropic grid (3 axes, 0.25 scale: +6 % scan)
 #endif
 #ifndef VPET_VOXS
-#define VPET_VOXS 0.25f
+#define VPET_VOXS 1.0f
 #endif
 #ifndef VPET_VOXS3
 #define VPET_VOXS3 VPET_VOXS  // scale of the third and fourth axes

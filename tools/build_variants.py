@@ -52,6 +52,13 @@ VARIANTS = {
     "quota0": ("VPET_QUOTA=0",),
     "rpair0": ("VPET_RPAIR=0",),
     "tr0": ("VPET_TREFRESH=0",),
+    "voxkey4": ("VPET_VOXKEY=4",),
+    "vk4s05": ("VPET_VOXKEY=4", "VPET_VOXS=0.5f"),
+    "vk4s1": ("VPET_VOXKEY=4", "VPET_VOXS=1.0f"),
+    "voxs05": ("VPET_VOXS=0.5f",),
+    "voxs1": ("VPET_VOXS=1.0f",),
+    "voxs0125": ("VPET_VOXS=0.125f",),
+    "rnst3": ("VPET_NST=3",),
     "tr1": ("VPET_TREFRESH=1",),
     "sheap1": ("VPET_SHEAP=1",),
     "h12m6": ("VPET_HEAD=12", "VPET_MINB_ROT=6"),
