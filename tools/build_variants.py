@@ -52,6 +52,8 @@ VARIANTS = {
     "quota0": ("VPET_QUOTA=0",),
     "rpair0": ("VPET_RPAIR=0",),
     "tr0": ("VPET_TREFRESH=0",),
+    "rnt128": ("VPET_NT=128",),
+    "rnt128m4": ("VPET_NT=128", "VPET_MINB_ROT=4"),
     "voxkey4": ("VPET_VOXKEY=4",),
     "vk4s05": ("VPET_VOXKEY=4", "VPET_VOXS=0.5f"),
     "vk4s1": ("VPET_VOXKEY=4", "VPET_VOXS=1.0f"),
