@@ -378,3 +378,38 @@ def test_two_contexts_one_process(tb_small, rt_small):
             np.testing.assert_array_equal(np.nan_to_num(ra[k]), np.nan_to_num(a_ref[k]), err_msg=k)
         for k in b_ref:
             np.testing.assert_array_equal(np.nan_to_num(rb[k]), np.nan_to_num(b_ref[k]), err_msg=k)
+
+
+def test_rotated_basis_adversarial_voxels(tb_small):
+    """The FP32 pass runs in the eigenbasis of the bank covariance with a tail bound after the first
+    coordinates.  Voxels built from the ORACLE's bank probe its edge cases: exact bank
+    curves (D = 0 for one draw), curves one FP32 ulp away, midpoints of two draws, far outliers,
+    constant and all-zero TACs.  The rotated default must equal the oracle and, byte for byte, the
+    frame-basis pass (ABC_FLAG_NO_REORDER keeps the frame basis)."""
+    from oracle import oracle as O
+    o = O.OracleContext(**tb_small.ctx_kwargs)
+    tb_small.setup(o)
+    bank = o.bank()
+    rng = np.random.default_rng(5)
+    rows = rng.choice(bank.shape[0], 12, replace=False)
+    b = bank[rows].astype(np.float32)
+    y = np.concatenate([
+        b[:4],                                                     # exact bank curves
+        np.nextafter(b[4:6], np.float32(np.inf)),                  # one ulp up, every frame
+        ((b[6:8].astype(np.float64) + b[8:10]) / 2).astype(np.float32),  # midpoints of two draws
+        b[10:12] * np.float32(25.0),                               # far outliers
+        np.full((1, b.shape[1]), np.float32(b.mean())),            # constant TAC
+        np.zeros((1, b.shape[1]), np.float32),                     # all zeros
+        tb_small.tacs[:50],                                        # ordinary voxels around them
+    ]).astype(np.float32)
+    g, _ = run_gpu(tb_small, tacs=y)
+    ref, _ = run_oracle(tb_small, tacs=y)
+    rep = compare(g, ref)
+    assert rep["matched"] >= y.shape[0] - 1, rep
+    # an exact bank curve accepts its own draw first, at distance 0
+    np.testing.assert_array_equal(g["acc_dist"][:4, 0], 0.0)
+    np.testing.assert_array_equal(np.asarray(g["acc_idx"][:4, 0]).astype(np.int64), rows[:4].astype(np.int64))
+    from paper_2603_14859_b200 import FLAG_NO_REORDER
+    fr, _ = run_gpu(tb_small, tacs=y, flags=FLAG_NO_REORDER)
+    for k in g:
+        np.testing.assert_array_equal(np.nan_to_num(g[k]), np.nan_to_num(fr[k]), err_msg=k)
