@@ -105,6 +105,8 @@ struct abc_ctx {
   cudaEvent_t tacs_ready = nullptr;
   cudaStream_t aux = nullptr;        // the order stage's basis computation, overlapped with its sorts
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  static constexpr int kOutChunks = 4;  // host outputs: K4 in chunks, each chunk's D2H overlapping the next
+  cudaEvent_t ev_chunk[kOutChunks] = {};
   bool ev_ok = false;
   int num_sms = 148;
 };
@@ -401,6 +403,9 @@ cudaError_t ensure_smem_attr(const void* func, size_t bytes) {
   return e;
 }
 
+// host outputs of at least this many voxels are reduced and copied back in chunks (overlap)
+constexpr uint64_t kChunkedOutMin = 1u << 18;
+
 // padded frame counts with a compiled FP32-pass instance (scan_kernels.cuh VPET_LP_LIST)
 static const uint32_t kLPs[] = {8, 12, 16, 20, 24, 28, 32, 36, 40, 44, 48, 56, 64, 80, 96, 128};
 bool scan_supported(uint32_t LP) {
@@ -512,7 +517,12 @@ abc_status abc_init(const abc_config* cfg, abc_ctx** out) {
       cudaEventCreateWithFlags(&c->tacs_ready, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      [&] {
+        for (auto& e : c->ev_chunk)
+          if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return true;
+        return false;
+      }()) {
     cudaStreamDestroy(c->own);
     delete c;
     return ABC_E_CUDA;
@@ -828,6 +838,7 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   }
 
   uint32_t launches = 0;
+  bool outs_copied = false;  // host outputs already copied chunk by chunk (K4 overlap)
   auto rec = [&](int k) {
     if (timing) cudaEventRecord(ctx->ev[k], st);
   };
@@ -1166,14 +1177,53 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
     rx.fb_list = nullptr;
     CK(launch_certify_reduce(rx, st));
     launches += 2;
-    if (split) {  // K4 for every voxel (certified or from a fallback tier)
+    if (split && host_out && J >= kChunkedOutMin) {
+      // K4 for every voxel, in chunks of voxels: the device-to-host copy of a chunk's outputs runs on
+      // the copy stream while K4 reduces the next chunk (the copies are joined before the call ends)
+      const int nch = abc_ctx::kOutChunks;
+      const uint64_t per = (J + nch - 1) / nch;
+      void* srcs[11] = {dout.prob, dout.preferred, dout.count, dout.mean, dout.sd, dout.q,
+                        dout.ki_mean, dout.ki_sd, dout.ki_q, dout.acc_idx, dout.acc_dist};
+      for (int c = 0; c < nch; ++c) {
+        const uint64_t v0 = uint64_t(c) * per, nv = std::min<uint64_t>(per, J - std::min<uint64_t>(J, v0));
+        if (nv == 0) break;
+        ReduceParams rq = rp;
+        rq.J = nv;
+        abc_result& o = rq.out;
+        if (o.prob) o.prob += v0 * M;
+        if (o.preferred) o.preferred += v0;
+        if (o.count) o.count += v0 * M;
+        if (o.mean) o.mean += v0 * P;
+        if (o.sd) o.sd += v0 * P;
+        if (o.q) o.q += v0 * P * 3;
+        if (o.ki_mean) o.ki_mean += v0;
+        if (o.ki_sd) o.ki_sd += v0;
+        if (o.ki_q) o.ki_q += v0 * 3;
+        if (o.acc_idx) o.acc_idx += v0 * n;
+        if (o.acc_dist) o.acc_dist += v0 * n;
+        CK(launch_reduce_accepted_lists(rq, ctx->hidx.as<uint32_t>() + v0 * n, ctx->hd.as<double>() + v0 * n,
+                                        ctx->flag.as<int>(), st));
+        ++launches;
+        CK(cudaEventRecord(ctx->ev_chunk[c], st));
+        CK(cudaStreamWaitEvent(ctx->copy, ctx->ev_chunk[c], 0));
+        for (int k = 0; k < 11; ++k) {
+          if (!od[k].user || !srcs[k]) continue;
+          const size_t row = od[k].bytes / J;
+          CK(cudaMemcpyAsync(static_cast<char*>(od[k].user) + v0 * row, static_cast<char*>(srcs[k]) + v0 * row, nv * row,
+                             cudaMemcpyDeviceToHost, ctx->copy));
+        }
+      }
+      CK(cudaEventRecord(ctx->ev_join, ctx->copy));
+      CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+      outs_copied = true;
+    } else if (split) {  // K4 for every voxel (certified or from a fallback tier)
       CK(launch_reduce_accepted_lists(rp, ctx->hidx.as<uint32_t>(), ctx->hd.as<double>(), ctx->flag.as<int>(), st));
       ++launches;
     }
     rec(EV_FB);
   }
   CK(cudaGetLastError());
-  if (host_out) {
+  if (host_out && !outs_copied) {
     void* srcs[11] = {dout.prob, dout.preferred, dout.count, dout.mean, dout.sd, dout.q,
                       dout.ki_mean, dout.ki_sd, dout.ki_q, dout.acc_idx, dout.acc_dist};
     for (int k = 0; k < 11; ++k)
@@ -1455,6 +1505,8 @@ void abc_destroy(abc_ctx* ctx) {
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  for (auto& e : ctx->ev_chunk)
+    if (e) cudaEventDestroy(e);
   if (ctx->tacs_ready) cudaEventDestroy(ctx->tacs_ready);
   delete ctx;
 }

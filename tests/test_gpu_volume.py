@@ -119,3 +119,18 @@ def test_continuous_phantom_fullN_oracle_parity():
     o = _oracle(p, p.tacs[idx])
     rep = compare({k: v[idx] for k, v in g.items()}, o)
     assert rep["matched"] >= len(idx) - 2, rep
+
+
+def test_host_outputs_chunked_copy_equal_device_outputs():
+    """Host output buffers of >= 2^18 voxels are reduced in chunks whose device-to-host copies
+    overlap the next chunk (api.cu): byte-identical to device outputs of the same call."""
+    import torch
+    from paper_2603_14859_b200 import AbcContext
+    p = S.config4_chunk(chunk=3, n_chunks=16, N=1_000_000, n=18)
+    assert p.J >= (1 << 18)
+    ctx = AbcContext(**p.ctx_kwargs)
+    p.setup(ctx)
+    host = ctx.run_voxels(p.tacs)  # numpy in -> numpy out (host outputs, chunked copies)
+    dev = ctx.run_voxels(torch.from_numpy(p.tacs).cuda())
+    for k, v in host.items():
+        np.testing.assert_array_equal(np.nan_to_num(v), np.nan_to_num(dev[k].cpu().numpy().view(v.dtype)), err_msg=k)
