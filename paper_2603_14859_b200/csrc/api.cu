@@ -682,7 +682,10 @@ abc_status abc_run_voxels(abc_ctx* ctx, const float* tacs, uint64_t J, uint32_t 
   // rotated scan basis: WL2, tree mode, frame reordering allowed, LP <= 96 (shared
   // memory of the basis and rotation kernels)
   static const bool rot_env = getenv("VPET_ROT") ? atoi(getenv("VPET_ROT")) != 0 : true;  // tuning knob
-  const bool rotated = rot_env && tree && ctx->dist_wl2() && !(ctx->cfg.flags & ABC_FLAG_NO_REORDER) && LP <= 96;
+  // and enough pairs to amortise the basis (config 2, 1e4 TACs x 2e5 draws: +12 ms of order stage
+  // for -2 ms of scan; the TB volume: 4.4e13 pairs)
+  const bool rotated = rot_env && tree && ctx->dist_wl2() && !(ctx->cfg.flags & ABC_FLAG_NO_REORDER) && LP <= 96 &&
+                       (double(J) * double(N) >= 1e11 || getenv("VPET_ROT_ALWAYS"));
   const size_t sort_tmp = tree ? order_sort_temp_bytes(N) : 0;
   // draw-range split of the tree scan (interleaved super-tiles): balances heavy voxels over SMs
   uint32_t nparts = 1;

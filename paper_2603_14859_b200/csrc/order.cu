@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(256) rot_kernel(const OrderParams p) {
     }
     __syncthreads();
   };
-  for (int sweep = 0; sweep < 30; ++sweep) {
+  for (int sweep = 0; sweep < 12; ++sweep) {  // a good basis suffices: exactness needs only orthogonality
     double off = 0.0, dia = 0.0;
     for (uint32_t e = tid; e < n * n; e += nt) {
       const double a = A[e];
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) rot_kernel(const OrderParams p) {
       else off += a * a;
     }
     block_sum2(off, dia, off, dia);
-    if (off <= 1e-30 * dia || off == 0.0) break;
+    if (off <= 1e-20 * dia || off == 0.0) break;
     for (uint32_t r = 0; r + 1 < n; ++r) {
       if (tid < n / 2) {
         // round-robin: position 0 holds index 0, position i >= 1 holds ((i - 1 + r) mod (n - 1)) + 1

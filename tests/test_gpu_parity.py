@@ -20,6 +20,15 @@ def tb_small():
     return S.config4_chunk(chunk=7, n_chunks=64, N=40_000, n=18, max_voxels=700)
 
 
+@pytest.fixture(params=[False, True], ids=["auto", "rotated"])
+def rot(request, monkeypatch):
+    """Run a test with the library's automatic choice of scan basis (small problems keep the frame
+    basis) and with the rotated eigenbasis forced (the bench volume's path)."""
+    if request.param:
+        monkeypatch.setenv("VPET_ROT_ALWAYS", "1")
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def rt_small():
     # config-2-shaped: lp-ntPET vs MRTM, 61 frames, PWL reference TAC
@@ -49,7 +58,7 @@ def test_bank_matches_oracle_rn32(cfg1, tb_small, rt_small):
         np.testing.assert_allclose(gb, ob, rtol=2.5e-7, atol=0)
 
 
-def test_config1_topn_wl2(cfg1):
+def test_config1_topn_wl2(cfg1, rot):
     g, gc = run_gpu(cfg1, flags=1)
     o, _ = run_oracle(cfg1)
     rep = compare(g, o)
@@ -60,7 +69,7 @@ def test_config1_topn_wl2(cfg1):
 
 @pytest.mark.parametrize("distance", ["L1", "WL2"])
 @pytest.mark.parametrize("weighted", [True, False])
-def test_config1_distances_and_weights(cfg1, distance, weighted):
+def test_config1_distances_and_weights(cfg1, distance, weighted, rot):
     p = cfg1.replace(distance=distance)
     if not weighted:
         import dataclasses
@@ -70,7 +79,7 @@ def test_config1_distances_and_weights(cfg1, distance, weighted):
     compare(g, o)
 
 
-def test_tb_model_selection(tb_small):
+def test_tb_model_selection(tb_small, rot):
     g, gc = run_gpu(tb_small)
     o, _ = run_oracle(tb_small)
     rep = compare(g, o)
@@ -83,7 +92,7 @@ def test_rt_model_selection(rt_small):
     compare(g, o)
 
 
-def test_brain_model_selection(brain_small):
+def test_brain_model_selection(brain_small, rot):
     """Config-3 shape: L = 90 (the widest frame count of the configs), MRTM vs lp-ntPET."""
     g, _ = run_gpu(brain_small)
     o, _ = run_oracle(brain_small)
@@ -92,7 +101,7 @@ def test_brain_model_selection(brain_small):
 
 
 @pytest.mark.parametrize("flags", [0x2, 0x8, 0x10, 0x8 | 0x10, 0x20, 0x20 | 0x8])
-def test_exact_noprune_noreorder_notree_identical(tb_small, flags):
+def test_exact_noprune_noreorder_notree_identical(tb_small, flags, rot):
     """ABC_FLAG_EXACT (pure FP64 scan), NO_PRUNE, NO_REORDER and NO_TREE (flat index-order scan) give
     bit-identical outputs to the default tree-ordered, bound-pruned FP32 pass."""
     sub = tb_small.subset(np.arange(130))
@@ -102,7 +111,7 @@ def test_exact_noprune_noreorder_notree_identical(tb_small, flags):
         np.testing.assert_array_equal(np.nan_to_num(base[k]), np.nan_to_num(alt[k]), err_msg=k)
 
 
-def test_eps_mode(cfg1):
+def test_eps_mode(cfg1, rot):
     """eps mode: accept D <= eps; moments from streaming sums."""
     o_top, _ = run_oracle(cfg1)
     eps = float(np.median(o_top["acc_dist"][:, -1]))
@@ -128,7 +137,7 @@ def test_wide_schedule_lp128():
 
 
 @pytest.mark.parametrize("N", [12345, 40_000 + 77])
-def test_ragged_draw_counts(tb_small, N):
+def test_ragged_draw_counts(tb_small, N, rot):
     """N not a multiple of the tile / super-tile / hyper-tile sizes; fewer hyper-tiles than parts."""
     half = N // 2
     models = [dict(m, n_draws=(half if k == 0 else N - half)) for k, m in enumerate(tb_small.ctx_kwargs["models"])]
@@ -211,7 +220,7 @@ def test_device_pointers_and_stream(tb_small):
         np.testing.assert_array_equal(np.nan_to_num(a), np.nan_to_num(b), err_msg=k)
 
 
-def test_forced_fallback_equals_oracle_and_default(tb_small):
+def test_forced_fallback_equals_oracle_and_default(tb_small, rot):
     """ABC_FLAG_FORCE_FALLBACK sends every voxel through the uncertified-voxel path (the on-device
     list, the warp-parallel exact FP64 scan and the exact reduction): same results as the oracle
     and bit-identical to the certified FP32 path."""
@@ -226,7 +235,7 @@ def test_forced_fallback_equals_oracle_and_default(tb_small):
     compare(fb, o)
 
 
-def test_exact_ties_fixed_parameter_prior(tb_small):
+def test_exact_ties_fixed_parameter_prior(tb_small, rot):
     """Exact D ties: model 0 has a fixed-parameter prior (lo == hi), so its whole
     block of draws simulates the same TAC; ties are resolved towards the lower draw index.  The
     fixed value is the truth of voxel 0, so the tied block fills voxel 0's accepted set."""
@@ -348,7 +357,7 @@ def test_large_n_cta_certification(tb_small, N, n, flags):
 
 
 @pytest.mark.parametrize("ell", [3.5, 14.0])
-def test_continuous_phantom_parity(ell):
+def test_continuous_phantom_parity(ell, rot):
     """Harder data: kinetic parameters as continuous fields over the whole prior range, low and high
     noise (synthetic.config4_continuous); exactness does not depend on clusterability."""
     p = S.config4_continuous(chunk=5, n_chunks=64, N=200_000, n=18, ell=ell, max_voxels=2000)
@@ -380,13 +389,14 @@ def test_two_contexts_one_process(tb_small, rt_small):
             np.testing.assert_array_equal(np.nan_to_num(rb[k]), np.nan_to_num(b_ref[k]), err_msg=k)
 
 
-def test_rotated_basis_adversarial_voxels(tb_small):
+def test_rotated_basis_adversarial_voxels(tb_small, monkeypatch):
     """The FP32 pass runs in the eigenbasis of the bank covariance with a tail bound after the first
     coordinates.  Voxels built from the ORACLE's bank probe its edge cases: exact bank
     curves (D = 0 for one draw), curves one FP32 ulp away, midpoints of two draws, far outliers,
     constant and all-zero TACs.  The rotated default must equal the oracle and, byte for byte, the
     frame-basis pass (ABC_FLAG_NO_REORDER keeps the frame basis)."""
     from oracle import oracle as O
+    monkeypatch.setenv("VPET_ROT_ALWAYS", "1")
     o = O.OracleContext(**tb_small.ctx_kwargs)
     tb_small.setup(o)
     bank = o.bank()
