@@ -52,6 +52,14 @@ VARIANTS = {
     "quota0": ("VPET_QUOTA=0",),
     "rpair0": ("VPET_RPAIR=0",),
     "tr0": ("VPET_TREFRESH=0",),
+    "rhinl": ("VPET_HEAP_INLINE=1",),
+    "rssort0": ("VPET_SSORT=0",),
+    "rqorder0": ("VPET_QORDER=0",),
+    "rhsort512": ("VPET_HSORTMAX=512",),
+    "rhsort128": ("VPET_HSORTMAX=128",),
+    "certminb6": ("CERT_MINB=6",),
+    "certminb8": ("CERT_MINB=8",),
+    "certminb3": ("CERT_MINB=3",),
     "rnt128": ("VPET_NT=128",),
     "rnt128m4": ("VPET_NT=128", "VPET_MINB_ROT=4"),
     "voxkey4": ("VPET_VOXKEY=4",),
