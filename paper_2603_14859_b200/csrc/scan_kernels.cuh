@@ -69,9 +69,15 @@ constexpr int T = kTile;
 #define VPET_RREFRESH 0  // and every VPET_RREFRESH rows inside a tile (0: off)
 #endif
 #ifndef VPET_HEAD
-#define VPET_HEAD 8  // rotated basis: coordinates evaluated before a row's first test (multiple of 4)
+#define VPET_HEAD 12  // rotated basis: coordinates evaluated before a row's first test (multiple of 4)
 #endif
 constexpr int kHead = VPET_HEAD;
+#ifndef VPET_BOXHEAD
+#define VPET_BOXHEAD 4  // coordinates of a box tested before its tail bound (<= kHead: rv starts at kHead);
+                        // measured 12 / 4 against 8 / 8: scan 144 -> 140 ms (16 / 4: 144, 16 / 8: 147)
+#endif
+constexpr int kBoxHead = VPET_BOXHEAD;
+static_assert(kBoxHead <= kHead && kBoxHead % 4 == 0, "the box head test must not overlap rv's coordinates");
 #ifndef VPET_SHEAP
 #define VPET_SHEAP 0  // keep the top of each candidate heap in shared memory (tree scan)
 #endif
@@ -783,14 +789,14 @@ __device__ __forceinline__ bool box_alive_rot(const Voxels<LP, R>& V, const Src 
   Acc acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc_zero(acc[r]);
-  bound_range<LP, R, 0, kHead>(V, box, box.off(LP), acc);
-  work += uint64_t(kHead) * R;
+  bound_range<LP, R, 0, kBoxHead>(V, box, box.off(LP), acc);
+  work += uint64_t(kBoxHead) * R;
   bool alive = false;
 #pragma unroll
   for (int r = 0; r < R; ++r) alive |= acc_total(acc[r]) < th[r];
   if (!__any_sync(0xffffffffu, alive)) return false;
-  bound_range<LP, R, kHead, LP>(V, box, box.off(LP), acc);
-  work += uint64_t(LP - kHead) * R;
+  bound_range<LP, R, kBoxHead, LP>(V, box, box.off(LP), acc);
+  work += uint64_t(LP - kBoxHead) * R;
   alive = false;
 #pragma unroll
   for (int r = 0; r < R; ++r) alive |= acc_total(acc[r]) < V.tau[r];

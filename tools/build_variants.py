@@ -52,6 +52,11 @@ VARIANTS = {
     "quota0": ("VPET_QUOTA=0",),
     "rpair0": ("VPET_RPAIR=0",),
     "tr0": ("VPET_TREFRESH=0",),
+    "boxhead4": ("VPET_BOXHEAD=4",),
+    "h16box4": ("VPET_HEAD=16", "VPET_BOXHEAD=4"),
+    "h16box8": ("VPET_HEAD=16", "VPET_BOXHEAD=8"),
+    "h12box8": ("VPET_HEAD=12", "VPET_BOXHEAD=8"),
+    "h12box4": ("VPET_HEAD=12", "VPET_BOXHEAD=4"),
     "rhinl": ("VPET_HEAP_INLINE=1",),
     "rssort0": ("VPET_SSORT=0",),
     "rqorder0": ("VPET_QORDER=0",),
