@@ -3,7 +3,7 @@ voxel subset of the whole TB volume at N = 1e7, the oracle's FP64 bank build tim
 per-voxel time extrapolated to the 4,441,800-voxel volume.  The oracle is test infrastructure and
 runs here as it stands (never tuned); this is a reported baseline, not a target.
 
-python tools/oracle_baseline.py [--voxels 1024] [--draws 10000000] [--out f.json]
+python tests/tools/oracle_baseline.py [--voxels 1024] [--draws 10000000] [--out f.json]
 """
 import argparse
 import json
@@ -11,7 +11,7 @@ import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 import numpy as np  # noqa: E402
 

@@ -7,13 +7,13 @@ decision, tiles of 32 rows in a Morton order of the first 4 principal projection
 voxel: row coordinate updates (a warp evaluates a tile's rows for all its voxels once the tile is
 alive for one) and tile-bound coordinate updates.
 
-python tools/sim_rotated_bound.py [--draws 1000000] [--warps 8] [--head 8]
+python tests/tools/sim_rotated_bound.py [--draws 1000000] [--warps 8] [--head 8]
 """
 import argparse
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 
 import synthetic as S  # noqa: E402
