@@ -53,6 +53,12 @@ VARIANTS = {
     "rpair0": ("VPET_RPAIR=0",),
     "tr0": ("VPET_TREFRESH=0",),
     "boxhead4": ("VPET_BOXHEAD=4",),
+    "href1": ("VPET_HREFRESH=1",),
+    "s1h3": ("VPET_REFRESH=1", "VPET_HREFRESH=3"),
+    "s3h3": ("VPET_REFRESH=3", "VPET_HREFRESH=3"),
+    "s1h7": ("VPET_REFRESH=1", "VPET_HREFRESH=7"),
+    "sref1": ("VPET_REFRESH=1",),
+    "href3": ("VPET_HREFRESH=3",),
     "h16box4": ("VPET_HEAD=16", "VPET_BOXHEAD=4"),
     "h16box8": ("VPET_HEAD=16", "VPET_BOXHEAD=8"),
     "h12box8": ("VPET_HEAD=12", "VPET_BOXHEAD=8"),
